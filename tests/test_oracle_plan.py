@@ -1,0 +1,253 @@
+"""Pins of the oracle's cost model, engine selection, task combination, ordering, hub
+sort and partitioning (§5-§6 of the paper) against SPEC's worked examples
+(tests/golden/spec_cost_examples.json), the Fig. 5 toy (tests/golden/fig5_toy.json), an
+independent Fraction restatement of the §5.1 prose with an arbitrary RTT, and
+brute-force restatements of H(v) ordering and the greedy partition sweep.  CPU only."""
+import json
+import os
+import random
+from fractions import Fraction
+from math import ceil
+
+import numpy as np
+import pytest
+
+import hytgen
+import oracle
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+ENG = {"none": oracle.NONE, "F": oracle.F, "C": oracle.C, "Z": oracle.Z, ".": oracle.NONE}
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ------------------------------------------------------------- SPEC worked examples
+
+def test_am_examples():
+    for ex in gold("spec_cost_examples.json")["am"]:
+        assert oracle.am(ex["start_byte"], ex["len_bytes"], ex["m"]) == ex["am"], ex["cite"]
+
+
+def test_tef_examples():
+    for ex in gold("spec_cost_examples.json")["tef"]:
+        assert oracle.tef(ex["t"], oracle.CostCfg(d1=ex["d1"])) == ex["tef"], ex["cite"]
+
+
+def test_tec_examples():
+    for ex in gold("spec_cost_examples.json")["tec"]:
+        cfg = oracle.CostCfg(d1=ex["d1"], d2=ex["d2"])
+        assert oracle.tec(ex["e"], ex["a"], cfg) == ex["tec"], ex["cite"]
+
+
+def test_select_examples():
+    for ex in gold("spec_cost_examples.json")["select"]:
+        cfg = oracle.CostCfg(d1=ex["d1"])
+        assert oracle.select(ex["t"], ex["e"], ex["a"], ex["z"], cfg) == ENG[ex["engine"]], ex["cite"]
+
+
+def test_combine_examples():
+    for ex in gold("spec_cost_examples.json")["combine"]:
+        p = [ENG[ch] for ch in ex["p"]]
+        assert oracle.combine(p, ex["k"]) == [tuple(u) for u in ex["units"]], ex["cite"]
+
+
+def test_order_examples():
+    for ex in gold("spec_cost_examples.json")["order"]:
+        units = [(i, i + 1) for i in range(len(ex["scores"]))]
+        assert oracle.order_units(units, ex["scores"]) == ex["order"], ex["cite"]
+
+
+def test_combine_unit_properties_random():
+    rng = random.Random(3)
+    for _ in range(500):
+        N = rng.randint(0, 40)
+        p = [rng.choice([0, 1, 1, 1, 2, 3]) for _ in range(N)]
+        k = rng.randint(1, 6)
+        units = oracle.combine(p, k)
+        covered = [i for a, b in units for i in range(a, b)]
+        assert covered == [i for i in range(N) if p[i] == 1]            # every F partition once
+        for a, b in units:
+            assert 1 <= b - a <= k and all(p[i] == 1 for i in range(a, b))
+            # maximality: a unit shorter than k ends at a run break
+            if b - a < k:
+                assert b == N or p[b] != 1
+
+
+# ------------------------------------------------------------- Fig. 5 toy
+
+def test_fig5_zero_copy_requests():
+    t = gold("fig5_toy.json")
+    deg = t["degrees"]
+    V = len(deg)
+    src = [v for v in range(V) for _ in range(deg[v])]
+    dst = [(v + j + 1) % V for v in range(V) for j in range(deg[v])]
+    g = hytgen.csr_from_edges(V, src, dst)
+    assert g.E == t["edges_total"]
+    cfg = oracle.CostCfg(d1=t["d1"], m=t["m"])
+    bounds = np.array([0, V], dtype=np.uint64)
+    res = {}
+    for name in ("green", "gray"):
+        active = np.zeros(V, dtype=np.uint8)
+        active[t[name]] = 1
+        pl = oracle.plan(g.off, active, bounds, cfg)
+        res[name] = pl
+        assert int(pl.z[0]) == t[name + "_requests"]
+        assert Fraction(int(pl.e[0]), int(pl.t[0])) == Fraction(1, 2)      # same active-edge ratio
+    assert int(res["green"].z[0]) > int(res["gray"].z[0])
+
+
+# ------------------------------------------------------------- §5.1 independent restatement
+
+def paper_rule(t, e, a, z, d1, d2=4, m=128, MR=256, rtt=Fraction(1)):
+    """§5.1 prose restated with decimals and an arbitrary RTT."""
+    alpha, beta, gamma = Fraction("0.8"), Fraction("0.4"), Fraction("0.625")
+    if e == 0:
+        return oracle.NONE
+    Tef = ceil(Fraction(t * d1, m) / MR) * rtt                          # Eq. 1
+    Tec = ceil(Fraction(e * d1 + a * d2, m) / MR) * rtt                  # Eq. 2, transfer term
+    rtt_zc = gamma * rtt + (1 - gamma) * Fraction(e, t) * rtt
+    Tiz = ceil(Fraction(z, MR)) * rtt_zc                                 # Eq. 3
+    if Tec < alpha * Tef and Tec < beta * Tiz:
+        return oracle.C
+    if Tiz < Tef:
+        return oracle.Z
+    return oracle.F
+
+
+def random_case(rng, d1):
+    t = rng.choice([rng.randint(1, 20000), rng.randint(1, 3_000_000), 8192 * rng.randint(1, 8)])
+    e = rng.choice([t, rng.randint(0, t), rng.randint(0, min(t, 300))])
+    a = 0 if e == 0 else rng.randint(1, e)
+    zmin = 0 if e == 0 else ceil(e * d1 / 128)
+    z = 0 if e == 0 else rng.randint(max(a, zmin), max(a, zmin) + 2 * a)
+    return t, e, a, z
+
+
+@pytest.mark.parametrize("d1", [4, 8])
+def test_select_matches_independent_restatement(d1):
+    rng = random.Random(d1)
+    cfg = oracle.CostCfg(d1=d1)
+    counts = {0: 0, 1: 0, 2: 0, 3: 0}
+    for _ in range(10000):
+        t, e, a, z = random_case(rng, d1)
+        want = paper_rule(t, e, a, z, d1)
+        assert oracle.select(t, e, a, z, cfg) == want, (t, e, a, z)
+        counts[want] += 1
+        # RTT can be arbitrarily specified: scaling changes no decision
+        rtt = Fraction(rng.randint(1, 997), rng.randint(1, 991))
+        assert paper_rule(t, e, a, z, d1, rtt=rtt) == want
+    assert min(counts[1], counts[2], counts[3]) > 200          # every engine exercised
+
+
+def test_select_saturation_tie_goes_to_filter():
+    # 256 aligned degree-32 vertices, all active: Tiz == Tef exactly -> F (prose, C1)
+    cfg = oracle.CostCfg(d1=4)
+    assert oracle.tef(8192, cfg) == 1 and oracle.nz(256, cfg) == 1
+    assert oracle.select(8192, 8192, 256, 256, cfg) == oracle.F
+
+
+# ------------------------------------------------------------- hub sort
+
+def test_hub_sort_star():
+    h = gold("hand_graphs.json")["hub_star"]
+    g = hytgen.csr_from_edges(h["V"], [e[0] for e in h["edges"]], [e[1] for e in h["edges"]])
+    new_id = oracle.hub_sort(g.off, g.nbr, Fraction(*h["frac"]))
+    assert int(new_id[0]) == h["new_id_of_0"]
+    assert new_id.tolist() == list(range(9))
+
+
+def test_hub_sort_fraction_zero_is_identity():
+    g = hytgen.rmat_csr(10, 1024, 8000, seed=2)
+    assert np.array_equal(oracle.hub_sort(g.off, g.nbr, Fraction(0)), np.arange(g.V))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_hub_sort_vs_fraction_restatement(seed):
+    g = hytgen.rmat_csr(10, 1000, 9000, seed=seed)
+    V = g.V
+    dout = np.diff(g.off.astype(np.int64))
+    din = np.bincount(g.nbr.astype(np.int64), minlength=V)
+    H = [Fraction(int(dout[v]) * int(din[v]), int(dout.max()) * int(din.max())) for v in range(V)]
+    frac = Fraction(8, 100)
+    h = ceil(frac * V)
+    top = sorted(range(V), key=lambda v: (-H[v], v))[:h]
+    rest = [v for v in range(V) if v not in set(top)]
+    want = np.empty(V, dtype=np.uint32)
+    for i, v in enumerate(top + rest):
+        want[v] = i
+    assert np.array_equal(oracle.hub_sort(g.off, g.nbr, frac), want)
+
+
+def test_relabel_is_isomorphism_and_results_invariant():
+    g = hytgen.rmat_csr(11, 2048, 20000, seed=4, weighted=True)
+    new_id = oracle.hub_sort(g.off, g.nbr)
+    off2, nbr2, w2 = oracle.relabel(g.off, g.nbr, g.w, new_id)
+    rows = np.repeat(np.arange(g.V), np.diff(g.off.astype(np.int64)))
+    rows2 = np.repeat(np.arange(g.V), np.diff(off2.astype(np.int64)))
+    e1 = sorted(zip(new_id[rows].tolist(), new_id[g.nbr].tolist(), g.w.tolist()))
+    e2 = sorted(zip(rows2.tolist(), nbr2.tolist(), w2.tolist()))
+    assert e1 == e2
+    src2 = int(new_id[0])
+    assert np.array_equal(oracle.bfs(off2, nbr2, src2)[new_id], oracle.bfs(g.off, g.nbr, 0))
+    assert np.array_equal(oracle.sssp(off2, nbr2, w2, src2)[new_id], oracle.sssp(g.off, g.nbr, g.w, 0))
+
+
+# ------------------------------------------------------------- partitioning
+
+def test_partition_examples():
+    hg = gold("hand_graphs.json")
+    h = hg["partition_chain"]
+    g = hytgen.csr_from_edges(h["V"], [e[0] for e in h["edges"]], [e[1] for e in h["edges"]])
+    b = oracle.partition(g.off, h["d1"], h["target_bytes"])
+    assert len(b) - 1 == h["n_partitions"] and b.tolist() == h["bounds"]
+    h = hg["partition_oversized"]
+    g = hytgen.csr_from_edges(h["V"], [e[0] for e in h["edges"]], [e[1] for e in h["edges"]])
+    b = oracle.partition(g.off, h["d1"], h["target_bytes"])
+    assert b[0] == 0 and b[1] == 1          # vertex 0 (10 edges = 40 B > 4 B) alone
+
+
+@pytest.mark.parametrize("target", [64, 4096, 65536])
+def test_partition_greedy_invariants(target):
+    g = hytgen.rmat_csr(12, 4096, 50000, seed=7)
+    for d1 in (4, 8):
+        b = oracle.partition(g.off, d1, target).astype(np.int64)
+        off = g.off.astype(np.int64)
+        assert b[0] == 0 and b[-1] == g.V and np.all(np.diff(b) > 0)
+        for i in range(len(b) - 1):
+            lo, hi = b[i], b[i + 1]
+            nbytes = (off[hi] - off[lo]) * d1
+            assert nbytes <= target or hi - lo == 1
+            if hi < g.V:     # greedy: the next vertex would not have fit
+                assert (off[hi + 1] - off[lo]) * d1 > target
+
+
+# ------------------------------------------------------------- Algorithm 1 aggregates
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_plan_aggregates_plain_definition(seed):
+    g = hytgen.rmat_csr(12, 4096, 60000, seed=seed)
+    rng = np.random.default_rng(seed)
+    for density in (0.001, 0.05, 0.6):
+        active = (rng.random(g.V) < density).astype(np.uint8)
+        for d1 in (4, 8):
+            cfg = oracle.CostCfg(d1=d1)
+            b = oracle.partition(g.off, d1, 16384)
+            pl = oracle.plan(g.off, active, b, cfg)
+            off = g.off.astype(np.int64)
+            deg = np.diff(off)
+            start = off[:-1] * d1
+            ln = deg * d1
+            lines = np.where(ln > 0, (start + ln - 1) // 128 - start // 128 + 1, 0)
+            req = np.where(ln > 0, lines, 0)        # ceil(len/m) + am == lines touched
+            for i in range(len(b) - 1):
+                sl = slice(int(b[i]), int(b[i + 1]))
+                act = active[sl] == 1
+                assert pl.t[i] == deg[sl].sum()
+                assert pl.a[i] == act.sum()
+                assert pl.e[i] == deg[sl][act].sum()
+                assert pl.z[i] == req[sl][act].sum()
+                assert pl.p[i] == oracle.select(int(pl.t[i]), int(pl.e[i]), int(pl.a[i]), int(pl.z[i]), cfg)
+            assert pl.units == oracle.combine(pl.p, 4)
