@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""bench.py -- HyTGraph hot path on B200: GTEPS and time-to-converge.
+
+Workload (BASELINE.json configs[1]): a Twitter-shaped RMAT graph (41.7M vertices,
+1.47B directed edges, u32 weights 1..63), SSSP from vertex 0 and delta-PageRank
+(eps 1e-6) on one B200 with the device budget capped at 16 GB and the edges in
+pinned host memory (the paper's storage split): every iteration each
+partition is served by the engine the section 5.1 cost model picks.
+
+One STEP = hyt_run(SSSP, 0) + hyt_run(PR) to convergence (inputs resident: the CSR
+in pinned host memory, offsets/vertex state in HBM).  value = whole-job GTEPS =
+(sum of out-degrees of reached vertices for SSSP + E for PR) / (time of both runs)
+(SURVEY C24 GTEPS_in).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config tw] [--shift S] [--budget-gb 16] [--algos sssp,pr]
+
+For N > 1 launch with torchrun (one rank per GPU, NCCL): every rank loads the
+graph, serves its contiguous range of partitions and the ranks reduce the pushed
+values once per iteration.  Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GTEPS and time-to-converge per algo at 1/2/4/8 B200, % HBM/PCIe peak"
+L2_NOTE = ("inputs larger than L2: edges live in pinned host memory (11.8 GB packed id+weight, "
+           "5.9 GB ids) and the vertex state (0.5 GB) exceeds the 126 MB L2")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="tw")
+    ap.add_argument("--shift", type=int, default=0, help="shrink the workload by 2**shift (debug only)")
+    ap.add_argument("--budget-gb", type=float, default=16.0)
+    ap.add_argument("--algos", default="sssp,pr")
+    ap.add_argument("--engine", default="hybrid")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-shift", type=int, default=6, help="oracle sample = the workload >> cpu_shift")
+    ap.add_argument("--json-out", default="")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = threading.Thread(target=self._loop, daemon=True)
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._th.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 5 + i and r[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# --------------------------------------------------------------------------- workload
+
+def make_graph(config: str, shift: int, weighted: bool):
+    import hytgen
+    t = time.time()
+    g = hytgen.make(config, shift=shift, weighted=weighted)
+    return g, time.time() - t
+
+
+def reached_edges(g, dist) -> int:
+    deg = np.diff(g.off.astype(np.int64))
+    return int(deg[dist != 0xFFFFFFFF].sum())
+
+
+def measured_h2d_gbs(device: int) -> float:
+    """Pinned host->device copy bandwidth on this box (host-link roofline denominator)."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=f"cuda:{device}")
+    for _ in range(2):
+        d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(4):
+        d.copy_(h, non_blocking=True)
+    e.record()
+    torch.cuda.synchronize()
+    gbs = 4 * n / (s.elapsed_time(e) / 1e3) / 1e9
+    del h, d
+    torch.cuda.empty_cache()
+    return gbs
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {"hbm_gbs": 6650.0, "fallback": True}
+
+
+# --------------------------------------------------------------------------- reference arm
+
+def cpu_oracle_sample(config: str, shift: int, algos, steps: int = 1):
+    """The CPU oracle (as it stands) on a bounded sample of the same workload."""
+    import oracle
+    g, _ = make_graph(config, shift, weighted=True)
+    edges = 0
+    secs = 0.0
+    for _ in range(steps):
+        for a in algos:
+            t = time.perf_counter()
+            if a == "sssp":
+                d = oracle.sssp(g.off, g.nbr, g.w, 0)
+                dt = time.perf_counter() - t
+                edges += reached_edges(g, d)
+            elif a == "bfs":
+                d = oracle.bfs(g.off, g.nbr, 0)
+                dt = time.perf_counter() - t
+                edges += reached_edges(g, d)
+            else:
+                oracle.pr_delta(g.off, g.nbr, eps=1e-6)
+                dt = time.perf_counter() - t
+                edges += g.E
+            secs += dt
+    return {"value": edges / secs / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+            "sample": f"{config}>>{shift} ({g.V} V, {g.E} E), {'+'.join(algos)}, single-threaded C oracle "
+                      f"(Dijkstra / sequential delta-PR eps 1e-6), {steps} step(s), {secs:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    algos = args.algos.split(",")
+    shift = max(args.shift, args.cpu_shift)
+    import oracle
+    g, _ = make_graph(args.config, shift, weighted=True)
+    times = []
+    edges_step = 0
+    for i in range(args.warmup + args.steps):
+        edges = 0
+        t0 = time.perf_counter()
+        for a in algos:
+            if a == "sssp":
+                edges += reached_edges(g, oracle.sssp(g.off, g.nbr, g.w, 0))
+            elif a == "bfs":
+                edges += reached_edges(g, oracle.bfs(g.off, g.nbr, 0))
+            else:
+                oracle.pr_delta(g.off, g.nbr, eps=1e-6)
+                edges += g.E
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            edges_step = edges
+    ms = 1e3 * float(np.mean(times))
+    val = edges_step / (ms / 1e3) / 1e9
+    sample = (f"{args.config}>>{shift} ({g.V} V, {g.E} E) -- bounded sample of the workload; "
+              f"single-threaded C oracle (Dijkstra, sequential delta-PR eps 1e-6)")
+    line = {"metric": METRIC, "value": val, "unit": "GTEPS", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.config} SSSP+PR (oracle sample {args.config}>>{shift})",
+                       "algos": algos},
+            "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    import paper_2208_14935_b200 as hyt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    algos = args.algos.split(",")
+    budget = int(args.budget_gb * (1 << 30))
+
+    # ---- inputs (host), generation not timed ----
+    if world > 1:
+        os.environ.setdefault("HYTGEN_THREADS", str(max(1, (os.cpu_count() or 8) // world)))
+    g, gen_s = make_graph(args.config, args.shift, weighted=True)
+    dstats = g.degree_stats()
+
+    def new_handle():
+        G = hyt.Graph(device=local, budget=budget)
+        if world > 1:
+            uid = [hyt.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            G.init_dist(rank, world, uid[0])
+        G.set("engine_mode", args.engine)
+        return G
+
+    G = new_handle()
+    t = time.time()
+    G.load(g.off, g.nbr, g.w)
+    load_s = time.time() - t
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step(H, out_bufs=None):
+        """One pass of the hot path: every algorithm to convergence."""
+        res = {}
+        for a in algos:
+            H.run(a, 0)
+            st = H.stats()
+            res[a] = st
+            if out_bufs is not None:
+                H.values_into(out_bufs[a])
+        return res
+
+    # ---- warm-up ----
+    out_bufs = {a: np.empty(g.V, dtype=np.float32 if a == "pr" else np.uint32) for a in algos}
+    for _ in range(args.warmup):
+        step(G)
+    # edges per step (GTEPS_in): reached out-degrees for SSSP/BFS, E for PR/CC
+    edges_per = {}
+    for a in algos:
+        G.run(a, 0)
+        if a in ("sssp", "bfs"):
+            edges_per[a] = reached_edges(g, G.values())
+        else:
+            edges_per[a] = g.E
+
+    # ---- timed region ----
+    cur = torch.cuda.current_stream()
+    times, per_algo_ms, launches = [], {a: [] for a in algos}, 0
+    eng_ms = np.zeros(8)
+    eng_launch = np.zeros(8, dtype=np.int64)
+    eng_chunks = np.zeros(8, dtype=np.int64)
+    eng_edges = np.zeros(8, dtype=np.int64)
+    link_bytes = 0
+    iters = {a: 0 for a in algos}
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            barrier()
+            t_ev = []
+            for a in algos:
+                s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s_ev.record(cur)
+                G.run(a, 0)                     # blocking: returns after its streams finished
+                e_ev.record(cur)
+                t_ev.append((a, s_ev, e_ev))
+                st = G.stats()
+                launches += st["kernel_launches"]
+                eng_ms += np.array(st["eng_ms"])
+                eng_launch += np.array(st["eng_launches"])
+                eng_chunks += np.array(st["eng_chunks"])
+                eng_edges += np.array(st["eng_edges"])
+                link_bytes += st["bytes_filter"] + st["bytes_compaction"] + st["bytes_zerocopy"]
+                iters[a] = st["iterations"]
+            barrier()
+            tot = 0.0
+            for a, s_ev, e_ev in t_ev:
+                ms = s_ev.elapsed_time(e_ev)
+                per_algo_ms[a].append(ms)
+                tot += ms
+            times.append(tot)
+    step_ms = float(np.mean(times))
+    if world > 1:
+        tt = torch.tensor([step_ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        step_ms = float(tt.item())
+    edges_step = sum(edges_per.values())
+    value = edges_step / (step_ms / 1e3) / 1e9
+
+    # ---- e2e: the public API with host buffers (load from host + run + results to host) ----
+    e2e = None
+    if args.e2e_steps > 0:
+        G.close()
+        e2e_ms = []
+        for _ in range(args.e2e_steps):
+            barrier()
+            s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s_ev.record(cur)
+            H = new_handle()
+            H.load(g.off, g.nbr, g.w)
+            step(H, out_bufs)
+            e_ev.record(cur)
+            barrier()
+            e2e_ms.append(s_ev.elapsed_time(e_ev))
+            H.close()
+        em = float(np.mean(e2e_ms))
+        if world > 1:
+            tt = torch.tensor([em], device=f"cuda:{local}")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            em = float(tt.item())
+        h2d = g.off.nbytes + g.nbr.nbytes + g.w.nbytes
+        e2e = {"value": edges_step / (em / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": em,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * g.V * len(algos)),
+               "includes": "hyt_load_csr from host arrays (pin + GPU hub sort + relabel) + runs + hyt_get_values"}
+    else:
+        G.close()
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel ----
+    pk = peaks()
+    hbm_peak = float(pk.get("hbm_gbs", 6650.0))
+    h2d_peak = measured_h2d_gbs(local)
+    tags = hyt.TAGS
+    d1 = {a: 8 if a == "sssp" else 4 for a in algos}
+    kernel_tags = [1, 2, 3, 4, 5]
+    dom = max(kernel_tags, key=lambda i: eng_ms[i]) if eng_ms[kernel_tags].sum() > 0 else 0
+    roof = None
+    if eng_launch[dom] > 0:
+        avg_s = eng_ms[dom] / 1e3 / eng_launch[dom]
+        if dom == 3:    # zero-copy: bound by the host link, algorithmic bytes = touched 128-B lines
+            alg_bytes = eng_chunks[dom] * 16 / eng_launch[dom]
+            roof = {"kernel": "k_relax<zerocopy>", "bound": "pcie", "achieved": alg_bytes / avg_s / 1e9,
+                    "peak": h2d_peak, "unit": "GB/s", "peak_source": "pinned H2D copy measured in this run"}
+        else:           # HBM-side relax: chunk bytes + 4 B destination read per edge
+            alg_bytes = (eng_chunks[dom] * 16 + eng_edges[dom] * 4) / max(1, eng_launch[dom])
+            roof = {"kernel": f"k_relax<{tags[dom]}>", "bound": "hbm", "achieved": alg_bytes / avg_s / 1e9,
+                    "peak": hbm_peak, "unit": "GB/s",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("fallback") else "")}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["avg_launch_ms"] = avg_s * 1e3
+        roof["launches"] = int(eng_launch[dom])
+        roof["share_of_kernel_time"] = float(eng_ms[dom] / max(1e-9, eng_ms[kernel_tags].sum()))
+    total_s = sum(times) / 1e3
+    host_link = {"bytes": int(link_bytes), "achieved": link_bytes / total_s / 1e9, "peak": h2d_peak,
+                 "unit": "GB/s", "frac": link_bytes / total_s / 1e9 / h2d_peak,
+                 "note": "algorithmic host-link bytes (filter spans + compacted chunks + zero-copy lines) / step time"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_oracle_sample(args.config, max(args.shift, args.cpu_shift), algos)
+        except Exception as ex:
+            cpu = {"error": repr(ex)}
+
+    per_algo = {}
+    for a in algos:
+        ms = float(np.mean(per_algo_ms[a]))
+        per_algo[a] = {"time_to_converge_s": ms / 1e3, "gteps": edges_per[a] / (ms / 1e3) / 1e9,
+                       "edges": int(edges_per[a]), "iterations": int(iters[a])}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32(sssp)+f32(pr)", "data": "synthetic",
+        "config": {"workload": f"{args.config}" + (f">>{args.shift}" if args.shift else "") +
+                   f": RMAT {g.V} V / {g.E} E directed, u32 weights 1..63; " + "+".join(algos) +
+                   " from vertex 0 (PR eps 1e-6)",
+                   "budget_gb": args.budget_gb, "engine_mode": args.engine, "partition_bytes": 32 << 20,
+                   "parallelism": f"vertex-range x{world}" if world > 1 else "single GPU",
+                   "l2": L2_NOTE, "degree_stats": dstats},
+        "per_algo": per_algo,
+        "roofline": roof,
+        "host_link": host_link,
+        "engine_ms": {tags[i]: float(eng_ms[i]) for i in range(7)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "setup_s": {"generate": gen_s, "load": load_s},
+    }
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.json_out:
+        with open(args.json_out, "w") as f:
+            f.write(s + "\n")
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,230 @@
+/*
+ * hyt.h -- C ABI of the B200-native HyTGraph hot path (libhyt.so).
+ *
+ * The library runs the per-iteration, frontier-driven push of HyTGraph
+ * (Wang et al., arXiv 2208.14935; "the paper", PAPER.md line numbers P:n) over a
+ * CSR whose vertex data lives on the GPU and whose edges live in pinned host
+ * memory.  Each iteration every vertex-range
+ * partition with active edges is served by the engine the paper's cost model
+ * picks (Eq. 1-3 and the section 5.1 rule; Algorithm 1):
+ *   - ExpTM-filter      : whole-partition async bulk copy + relax
+ *   - ExpTM-compaction  : host gather of the active edge lists + one bulk copy
+ *                         + relax over the compacted lists
+ *   - ImpTM-zero-copy   : relax reading edges straight from mapped host memory
+ *                         with aligned 128-byte-line loads
+ * combined into tasks, ordered by contribution and
+ * overlapped on several CUDA streams.
+ *
+ * Conventions (all calls):
+ *   - Every function returns HYT_OK (0) or a negative HYT_E* code; it never
+ *     throws across the ABI.  hyt_last_error() returns a thread-local message
+ *     describing the most recent failure of this thread.
+ *   - Pointers named *_host are host pointers; nothing in this header is a
+ *     device pointer except the optional arena of hyt_set_device_arena().
+ *   - Vertex ids in every argument and result are the CALLER's ids ("original"
+ *     ids); the hub-sorted internal order is never exposed except by
+ *     hyt_get_perm().
+ *   - A handle is not thread-safe: one thread at a time per handle.
+ *   - One handle drives one GPU (the device given to hyt_init); in a multi-GPU
+ *     job each process owns one handle and one GPU (hyt_init_dist).
+ *   - There is no CPU fallback: if the CUDA device is unavailable every call
+ *     that needs it fails with HYT_ECUDA.
+ */
+#ifndef HYT_H
+#define HYT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ---- */
+#define HYT_OK        0
+#define HYT_EINVAL   -1   /* bad argument or malformed CSR                         */
+#define HYT_ENOMEM   -2   /* device budget or pinned host memory exhausted          */
+#define HYT_ECUDA    -3   /* CUDA runtime error (message in hyt_last_error)         */
+#define HYT_ESTATE   -4   /* call out of order (e.g. run before load)              */
+#define HYT_ENCCL    -5   /* NCCL error in the multi-GPU exchange                   */
+
+/* ---- algorithms ---- */
+#define HYT_BFS   0       /* levels from source, push lvl+1, merge min (u32)       */
+#define HYT_SSSP  1       /* distances from source, push dist+w, merge min (u32)   */
+#define HYT_CC    2       /* min original id per component, on symmetric graphs    */
+#define HYT_PR    3       /* delta-PageRank, unnormalised, f32             */
+
+/* ---- load flags ---- */
+#define HYT_NO_HUBSORT 1u /* keep the caller's vertex order (skip P:452-462)        */
+
+/* ---- engine modes (hyt_set_param "engine_mode") ---- */
+#define HYT_MODE_HYBRID     0  /* the paper: per-partition cost-model selection    */
+#define HYT_MODE_FILTER     1  /* every active partition -> ExpTM-filter           */
+#define HYT_MODE_COMPACTION 2  /* every active partition -> ExpTM-compaction       */
+#define HYT_MODE_ZEROCOPY   3  /* every active partition -> ImpTM-zero-copy        */
+#define HYT_MODE_RESIDENT   4  /* edges copied once into device memory (build     */
+                               /* extension); needs budget >= edges     */
+
+/* ---- engine ids in plans (hyt_debug_plan) ---- */
+#define HYT_ENG_NONE 0
+#define HYT_ENG_F    1
+#define HYT_ENG_C    2
+#define HYT_ENG_Z    3
+#define HYT_ENG_R    4
+
+typedef struct hyt_graph hyt_graph;
+
+/* Per-run statistics (hyt_get_stats).  Bytes are algorithmic host-link bytes:
+ * filter = whole copied spans (Eq. 1), compaction = copied compacted chunks,
+ * zero-copy = touched 128-byte lines (Eq. 3 requests x m). */
+typedef struct {
+    uint64_t iterations;
+    uint64_t time_ns;              /* hyt_run wall time (host clock)              */
+    uint64_t edges_relaxed;        /* sum over tasks of active edges pushed       */
+    uint64_t edges_reached;        /* sum of out-degrees of vertices with a value */
+    uint64_t bytes_filter, bytes_compaction, bytes_zerocopy;
+    uint64_t parts_filter, parts_compaction, parts_zerocopy, parts_resident;
+    uint64_t units_filter;         /* combined filter tasks                */
+    uint64_t device_bytes_peak;    /* arena high-water mark (<= budget)           */
+    uint64_t num_partitions;
+    double   kernel_ms;            /* sum of relax-kernel times (CUDA events)     */
+    double   copy_ms;              /* sum of H2D copy times (CUDA events)         */
+    double   plan_ms;              /* activity/selection/fill kernels             */
+    double   gather_ms;            /* host compaction gather (wall)               */
+    uint64_t kernel_launches;      /* CUDA kernels this library launched in the run */
+    /* Per activity tag: 0 plan (activity/selection/fill), 1 filter relax,
+     * 2 compaction relax, 3 zero-copy relax, 4 resident relax, 5 filter
+     * recompute pass, 6 host-to-device copies.  Times are sums of per-launch
+     * CUDA-event durations on the launching stream. */
+    double   eng_ms[8];
+    uint64_t eng_launches[8];
+    uint64_t eng_chunks[8];        /* 16-byte edge chunks read by the relax launches */
+    uint64_t eng_edges[8];         /* active edges pushed by the relax launches      */
+} hyt_stats;
+
+/* One row per iteration (hyt_get_iter_log), the Fig. 7 / Table VI analog. */
+typedef struct {
+    uint64_t iteration;
+    uint64_t active_vertices, active_edges;
+    uint32_t parts_f, parts_c, parts_z, parts_r;
+    uint32_t units_f, pad;
+    uint64_t bytes_f, bytes_c, bytes_z;
+    double   ms;                   /* wall time of the iteration                  */
+} hyt_iter;
+
+/* Create a handle bound to CUDA device `device`.  No device memory is
+ * allocated until hyt_load_csr.  Errors: HYT_ECUDA (no such device). */
+int hyt_init(hyt_graph **g, int device);
+
+/* Cap every device allocation the handle makes (load and run) at `bytes`
+ * (budget = vertex state + staging + optional resident edges).
+ * 0 = no cap.  Must be called before hyt_load_csr.  The paper assumes vertex
+ * data fits: a run whose vertex state exceeds the budget fails with
+ * HYT_ENOMEM; staging shrinks to what is left. */
+int hyt_set_device_budget(hyt_graph *g, uint64_t bytes);
+
+/* Optional: sub-allocate everything from a caller-owned device block (e.g. a
+ * torch tensor) instead of cudaMalloc; sets the budget to `bytes`.  The block
+ * must stay alive until hyt_free.  Call before hyt_load_csr. */
+int hyt_set_device_arena(hyt_graph *g, void *dptr, uint64_t bytes);
+
+/* Load a CSR graph.
+ *   V, E          : vertices (< 2^32) and stored edges.
+ *   off_host      : u64[V+1], off[0]=0, non-decreasing, off[V]=E.
+ *   nbr_host      : u32[E] neighbour ids (< V).
+ *   w_host        : u32[E] edge weights (SSSP) or NULL.
+ *   flags         : HYT_NO_HUBSORT or 0.
+ * The library hub-sorts (top ceil(0.08 V) by D_o*D_i first,
+ * descending, ties by id; the rest in natural order), relabels on the GPU and
+ * stores the edges in library-owned pinned, mapped host memory (ids u32[E];
+ * with weights also packed (id | w<<32) u64[E]).  The caller's arrays are
+ * only read during the call; they are page-locked (cudaHostRegister) for its
+ * duration, so they must not already be registered by someone else unless
+ * they are cudaHostAlloc memory.  Errors: HYT_EINVAL (malformed CSR),
+ * HYT_ENOMEM (pinning or budget), HYT_ECUDA, HYT_ESTATE (already loaded). */
+int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
+                 const uint32_t *nbr_host, const uint32_t *w_host, uint32_t flags);
+
+/* Set a run parameter.  Keys (defaults in brackets):
+ *   alpha [0.8], beta [0.4]; gamma [0.625]; m [128],
+ *   mr [256]; d2 [4]; k [4];
+ *   partition_bytes [33554432]; hub_fraction [0.08] (load time);
+ *   streams [4]; engine_mode [HYT_MODE_HYBRID]; priority [-1 = auto:
+ *   delta for PR, hub otherwise; 0 none, 1 hub, 2 delta];
+ *   recompute [1] (process a loaded filter unit once more);
+ *   damping [0.85], epsilon [1e-6], max_iters [1000] (PR);
+ *   gather_threads [0 = all cores]; compaction_buffer_bytes [0 = auto].
+ * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
+int hyt_set_param(hyt_graph *g, const char *key, double value);
+
+/* Run `algo` from `source` (caller id; ignored by CC and PR) to convergence:
+ * until no vertex is active, for PR until no delta exceeds epsilon or
+ * max_iters.  Blocking; results stay on the device.  Errors: HYT_EINVAL
+ * (source >= V, SSSP without weights), HYT_ESTATE (no graph), HYT_ENOMEM
+ * (vertex state over budget), HYT_ECUDA, HYT_ENCCL. */
+int hyt_run(hyt_graph *g, int algo, uint64_t source);
+
+/* Copy the last run's results, indexed by caller id, into out_host:
+ * u32[V] for BFS/SSSP (0xFFFFFFFF = unreachable) and CC (minimum caller id of
+ * the component), f32[V] for PR.  count must equal V.  In a multi-GPU job
+ * every rank receives all V values.  Errors: HYT_ESTATE (no run yet),
+ * HYT_EINVAL (count != V). */
+int hyt_get_values(hyt_graph *g, void *out_host, uint64_t count);
+
+/* Statistics of the last run. */
+int hyt_get_stats(hyt_graph *g, hyt_stats *s);
+
+/* Per-iteration rows of the last run: copies min(cap, n) rows, sets *n. */
+int hyt_get_iter_log(hyt_graph *g, hyt_iter *rows, uint64_t cap, uint64_t *n);
+
+/* The load-time permutation: new_id_host[caller id] = internal id (u32[V]). */
+int hyt_get_perm(hyt_graph *g, uint32_t *new_id_host, uint64_t count);
+
+/* Debug/test hook for plan parity: for algorithm `algo` (fixes
+ * d1), evaluate Algorithm 1 on the GPU for the frontier given as a u8[V]
+ * array in CALLER ids, without running anything.  Outputs, each sized by the
+ * partition count (query it first with all output pointers NULL):
+ *   *num_parts; bounds_host u64[N+1] (internal vertex ids); t,e,a,z u64[N];
+ *   p_host u8[N] (HYT_ENG_*).  Errors as hyt_run. */
+int hyt_debug_plan(hyt_graph *g, int algo, const uint8_t *active_host, uint64_t *num_parts,
+                   uint64_t *bounds_host, uint64_t *t_host, uint64_t *e_host,
+                   uint64_t *a_host, uint64_t *z_host, uint8_t *p_host);
+
+/* Task combination (Alg. 1 L14-24 with the corrected loop), the
+ * host routine the scheduler uses, exposed for CPU tests: splits each maximal
+ * run of consecutive HYT_ENG_F entries of p[0..n) into units of <= k.
+ * units_host receives pairs (first, one-past-last); returns the unit count
+ * (>= 0) or HYT_EINVAL.  Needs no GPU. */
+int64_t hyt_combine(const uint8_t *p_host, uint64_t n, uint64_t k, uint64_t *units_host);
+
+/* Engine selection for one partition (section 5.1), the exact
+ * integer rule the GPU selection kernel evaluates, exposed for CPU tests.
+ * Inputs: t = sum of out-degrees of the partition, e = active edges,
+ * a = active vertices, z = zero-copy requests; d1 bytes per edge record;
+ * the remaining constants come from the handle's parameters (or defaults
+ * when g == NULL).  Returns HYT_ENG_* or HYT_EINVAL.  Needs no GPU. */
+int hyt_select_engine(const hyt_graph *g, uint64_t t, uint64_t e, uint64_t a, uint64_t z,
+                      uint64_t d1);
+
+/* ---- multi-GPU (vertex-range sharding, NCCL over NVLink) ----
+ * Call after hyt_init and before hyt_load_csr on every rank.  nccl_uid is the
+ * 128-byte ncclUniqueId created by rank 0 (hyt_nccl_unique_id) and broadcast
+ * by the caller (e.g. torch.distributed).  Every rank then loads the SAME
+ * graph; each rank serves its own contiguous range of partitions and the
+ * ranks exchange pushed values once per iteration (min for BFS/SSSP/CC, sum
+ * for PR deltas).  Errors: HYT_ENCCL. */
+int hyt_nccl_unique_id(void *uid_out_128_bytes);
+int hyt_init_dist(hyt_graph *g, int rank, int world, const void *nccl_uid_128_bytes);
+
+/* Release everything (device arena, pinned host memory, streams, NCCL). */
+void hyt_free(hyt_graph *g);
+
+/* Thread-local message of this thread's last failure ("" if none). */
+const char *hyt_last_error(void);
+
+/* Library version string. */
+const char *hyt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYT_H */

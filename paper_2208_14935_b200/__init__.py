@@ -1,0 +1,232 @@
+"""paper_2208_14935_b200 -- B200-native HyTGraph hot path (arXiv 2208.14935).
+
+A thin ctypes binding over the C ABI in include/hyt.h (libhyt.so, built for
+sm_100a).  Every step of the path runs in the library's CUDA kernels; this module
+only marshals arguments.  There is no CPU fallback: importing works without a GPU
+(the CPU test suite checks the exports), but every call that needs the device
+fails loudly with HytError, and a missing libhyt.so raises at import time.
+
+PyTorch is used only for plumbing: an optional device arena (a torch tensor the
+library sub-allocates from) and torch.distributed for the NCCL unique-id broadcast.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libhyt.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "hyt.h")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `make` or __graft_entry__.build() "
+                      "(there is no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+
+HYT_OK, HYT_EINVAL, HYT_ENOMEM, HYT_ECUDA, HYT_ESTATE, HYT_ENCCL = 0, -1, -2, -3, -4, -5
+HYT_BFS, HYT_SSSP, HYT_CC, HYT_PR = 0, 1, 2, 3
+ALGOS = {"bfs": HYT_BFS, "sssp": HYT_SSSP, "cc": HYT_CC, "pr": HYT_PR}
+HYT_NO_HUBSORT = 1
+MODES = {"hybrid": 0, "filter": 1, "compaction": 2, "zerocopy": 3, "resident": 4}
+HYT_ENG_NONE, HYT_ENG_F, HYT_ENG_C, HYT_ENG_Z, HYT_ENG_R = 0, 1, 2, 3, 4
+TAGS = ["plan", "filter", "compaction", "zerocopy", "resident", "recompute", "copy", "unused"]
+INF32 = 0xFFFFFFFF
+
+
+class hyt_stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "iterations", "time_ns", "edges_relaxed", "edges_reached", "bytes_filter", "bytes_compaction",
+        "bytes_zerocopy", "parts_filter", "parts_compaction", "parts_zerocopy", "parts_resident",
+        "units_filter", "device_bytes_peak", "num_partitions")] + [
+        (n, ctypes.c_double) for n in ("kernel_ms", "copy_ms", "plan_ms", "gather_ms")] + [
+        ("kernel_launches", ctypes.c_uint64), ("eng_ms", ctypes.c_double * 8),
+        ("eng_launches", ctypes.c_uint64 * 8), ("eng_chunks", ctypes.c_uint64 * 8), ("eng_edges", ctypes.c_uint64 * 8)]
+
+
+class hyt_iter(ctypes.Structure):
+    _fields_ = [("iteration", ctypes.c_uint64), ("active_vertices", ctypes.c_uint64),
+                ("active_edges", ctypes.c_uint64), ("parts_f", ctypes.c_uint32), ("parts_c", ctypes.c_uint32),
+                ("parts_z", ctypes.c_uint32), ("parts_r", ctypes.c_uint32), ("units_f", ctypes.c_uint32),
+                ("pad", ctypes.c_uint32), ("bytes_f", ctypes.c_uint64), ("bytes_c", ctypes.c_uint64),
+                ("bytes_z", ctypes.c_uint64), ("ms", ctypes.c_double)]
+
+
+_vp, _u64, _i32, _u32 = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32
+_SIGS = {
+    "hyt_init": ([ctypes.POINTER(_vp), _i32], _i32),
+    "hyt_set_device_budget": ([_vp, _u64], _i32),
+    "hyt_set_device_arena": ([_vp, _vp, _u64], _i32),
+    "hyt_load_csr": ([_vp, _u64, _u64, _vp, _vp, _vp, _u32], _i32),
+    "hyt_set_param": ([_vp, ctypes.c_char_p, ctypes.c_double], _i32),
+    "hyt_run": ([_vp, _i32, _u64], _i32),
+    "hyt_get_values": ([_vp, _vp, _u64], _i32),
+    "hyt_get_stats": ([_vp, ctypes.POINTER(hyt_stats)], _i32),
+    "hyt_get_iter_log": ([_vp, _vp, _u64, ctypes.POINTER(_u64)], _i32),
+    "hyt_get_perm": ([_vp, _vp, _u64], _i32),
+    "hyt_debug_plan": ([_vp, _i32, _vp, ctypes.POINTER(_u64), _vp, _vp, _vp, _vp, _vp, _vp], _i32),
+    "hyt_combine": ([_vp, _u64, _u64, _vp], ctypes.c_int64),
+    "hyt_select_engine": ([_vp, _u64, _u64, _u64, _u64, _u64], _i32),
+    "hyt_nccl_unique_id": ([_vp], _i32),
+    "hyt_init_dist": ([_vp, _i32, _i32, _vp], _i32),
+    "hyt_free": ([_vp], None),
+    "hyt_last_error": ([], ctypes.c_char_p),
+    "hyt_version": ([], ctypes.c_char_p),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+    globals()[_name] = _f          # same names as the C ABI
+
+
+def declared_symbols() -> list:
+    """Every function include/hyt.h declares (used by the CPU export test)."""
+    with open(HEADER_PATH) as f:
+        txt = f.read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(hyt_[a-z_0-9]+)\s*\(", txt, re.M)))
+
+
+class HytError(RuntimeError):
+    def __init__(self, code: int, where: str):
+        msg = hyt_last_error().decode(errors="replace")
+        super().__init__(f"{where} failed with code {code}: {msg}")
+        self.code = code
+
+
+def check(rc: int, where: str) -> int:
+    if rc < 0:
+        raise HytError(rc, where)
+    return rc
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+class Graph:
+    """One handle = one GPU.  Typical use:
+
+        g = Graph(device=0, budget=16 << 30)
+        g.load(off, nbr, w)                 # host numpy arrays (caller ids)
+        g.run("sssp", 0)
+        dist = g.values()                   # u32[V] by caller id
+    """
+
+    def __init__(self, device: int = 0, budget: int = 0, arena: str | None = None, **params):
+        h = _vp()
+        check(hyt_init(ctypes.byref(h), device), "hyt_init")
+        self.h = h
+        self.V = 0
+        self._arena_tensor = None
+        if arena == "torch" and budget:
+            import torch
+            self._arena_tensor = torch.empty(budget, dtype=torch.uint8, device=f"cuda:{device}")
+            check(hyt_set_device_arena(h, self._arena_tensor.data_ptr(), budget), "hyt_set_device_arena")
+        elif budget:
+            check(hyt_set_device_budget(h, budget), "hyt_set_device_budget")
+        for k, v in params.items():
+            self.set(k, v)
+
+    def set(self, key: str, value) -> None:
+        if key == "engine_mode" and isinstance(value, str):
+            value = MODES[value]
+        if key == "priority" and isinstance(value, str):
+            value = {"auto": -1, "none": 0, "hub": 1, "delta": 2}[value]
+        check(hyt_set_param(self.h, key.encode(), float(value)), f"hyt_set_param({key})")
+
+    def init_dist(self, rank: int, world: int, uid: bytes) -> None:
+        buf = ctypes.create_string_buffer(bytes(uid), 128)
+        check(hyt_init_dist(self.h, rank, world, buf), "hyt_init_dist")
+
+    def load(self, off, nbr, w=None, hubsort: bool = True) -> None:
+        off = np.ascontiguousarray(off, dtype=np.uint64)
+        nbr = np.ascontiguousarray(nbr, dtype=np.uint32)
+        if w is not None:
+            w = np.ascontiguousarray(w, dtype=np.uint32)
+        V = len(off) - 1
+        E = int(off[-1]) if V >= 0 else 0
+        check(hyt_load_csr(self.h, V, E, _ptr(off), _ptr(nbr) if E else None, _ptr(w) if w is not None else None,
+                           0 if hubsort else HYT_NO_HUBSORT), "hyt_load_csr")
+        self.V = V
+
+    def run(self, algo, source: int = 0) -> None:
+        a = ALGOS[algo] if isinstance(algo, str) else int(algo)
+        check(hyt_run(self.h, a, source), "hyt_run")
+        self._algo = a
+
+    def values(self) -> np.ndarray:
+        out = np.empty(self.V, dtype=np.float32 if self._algo == HYT_PR else np.uint32)
+        check(hyt_get_values(self.h, _ptr(out), self.V), "hyt_get_values")
+        return out
+
+    def values_into(self, out: np.ndarray) -> np.ndarray:
+        check(hyt_get_values(self.h, _ptr(out), self.V), "hyt_get_values")
+        return out
+
+    def stats(self) -> dict:
+        s = hyt_stats()
+        check(hyt_get_stats(self.h, ctypes.byref(s)), "hyt_get_stats")
+        out = {}
+        for n, _ in hyt_stats._fields_:
+            v = getattr(s, n)
+            out[n] = list(v) if n.startswith("eng_") else v
+        return out
+
+    def iter_log(self) -> list:
+        n = _u64()
+        check(hyt_get_iter_log(self.h, None, 0, ctypes.byref(n)), "hyt_get_iter_log")
+        rows = (hyt_iter * max(1, n.value))()
+        check(hyt_get_iter_log(self.h, ctypes.cast(rows, _vp), n.value, ctypes.byref(n)), "hyt_get_iter_log")
+        return [{f: getattr(rows[i], f) for f, _ in hyt_iter._fields_ if f != "pad"} for i in range(n.value)]
+
+    def perm(self) -> np.ndarray:
+        out = np.empty(self.V, dtype=np.uint32)
+        check(hyt_get_perm(self.h, _ptr(out), self.V), "hyt_get_perm")
+        return out
+
+    def debug_plan(self, algo, active: np.ndarray) -> dict:
+        a = ALGOS[algo] if isinstance(algo, str) else int(algo)
+        active = np.ascontiguousarray(active, dtype=np.uint8)
+        n = _u64()
+        check(hyt_debug_plan(self.h, a, _ptr(active), ctypes.byref(n), None, None, None, None, None, None),
+              "hyt_debug_plan")
+        N = n.value
+        b = np.empty(N + 1, dtype=np.uint64)
+        t, e, av, z = (np.empty(N, dtype=np.uint64) for _ in range(4))
+        p = np.empty(N, dtype=np.uint8)
+        check(hyt_debug_plan(self.h, a, _ptr(active), ctypes.byref(n), _ptr(b), _ptr(t), _ptr(e), _ptr(av),
+                             _ptr(z), _ptr(p)), "hyt_debug_plan")
+        return {"bounds": b, "t": t, "e": e, "a": av, "z": z, "p": p}
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            hyt_free(self.h)
+            self.h = None
+        self._arena_tensor = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def combine(p, k: int = 4) -> list:
+    p = np.ascontiguousarray(p, dtype=np.uint8)
+    units = np.empty(2 * len(p) + 2, dtype=np.uint64)
+    n = check(hyt_combine(_ptr(p) if len(p) else None, len(p), k, _ptr(units)), "hyt_combine")
+    return [(int(units[2 * j]), int(units[2 * j + 1])) for j in range(n)]
+
+
+def select_engine(t: int, e: int, a: int, z: int, d1: int) -> int:
+    return check(hyt_select_engine(None, t, e, a, z, d1), "hyt_select_engine")
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(hyt_nccl_unique_id(buf), "hyt_nccl_unique_id")
+    return buf.raw

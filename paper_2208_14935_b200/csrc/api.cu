@@ -1,0 +1,190 @@
+// api.cu -- the extern "C" boundary (include/hyt.h).  Every entry point catches
+// everything and returns an HYT_E* code; messages go to a thread-local buffer.
+#include <cstring>
+#include <string>
+#include "graph.h"
+
+namespace hyt {
+static thread_local std::string t_err;
+void set_error(const std::string &msg) { t_err = msg; }
+const char *get_error() { return t_err.c_str(); }
+}  // namespace hyt
+
+using namespace hyt;
+
+#define HYT_GUARD(...)                                                    \
+    try {                                                                  \
+        __VA_ARGS__;                                                       \
+        return HYT_OK;                                                     \
+    } catch (const Err &e) {                                               \
+        set_error(e.msg);                                                  \
+        return e.code;                                                     \
+    } catch (const std::exception &e) {                                   \
+        set_error(std::string("internal: ") + e.what());                   \
+        return HYT_ECUDA;                                                  \
+    } catch (...) {                                                        \
+        set_error("internal: unknown exception");                          \
+        return HYT_ECUDA;                                                  \
+    }
+
+extern "C" {
+
+const char *hyt_version(void) { return "hyt-b200 0.1 (sm_100a)"; }
+const char *hyt_last_error(void) { return get_error(); }
+
+int hyt_init(hyt_graph **out, int device) {
+    HYT_GUARD({
+        HYT_REQUIRE(out != nullptr, HYT_EINVAL, "null handle pointer");
+        *out = nullptr;
+        int n = 0;
+        HYT_CUDA(cudaGetDeviceCount(&n));
+        HYT_REQUIRE(device >= 0 && device < n, HYT_ECUDA, "no CUDA device " + std::to_string(device));
+        HYT_CUDA(cudaSetDevice(device));
+        hyt_graph *g = new hyt_graph();
+        g->device = device;
+        cudaError_t e = cudaStreamCreateWithFlags(&g->main, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { delete g; HYT_CUDA(e); }
+        *out = g;
+    })
+}
+
+int hyt_set_device_budget(hyt_graph *g, uint64_t bytes) {
+    HYT_GUARD({
+        HYT_REQUIRE(g, HYT_EINVAL, "null handle");
+        HYT_REQUIRE(!g->loaded, HYT_ESTATE, "set the budget before hyt_load_csr");
+        HYT_REQUIRE(!g->arena.ext, HYT_ESTATE, "an external arena is set");
+        g->arena.budget = bytes;
+    })
+}
+
+int hyt_set_device_arena(hyt_graph *g, void *dptr, uint64_t bytes) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && dptr && bytes, HYT_EINVAL, "bad arena");
+        HYT_REQUIRE(!g->loaded && g->arena.blocks.empty(), HYT_ESTATE, "set the arena before hyt_load_csr");
+        g->arena.ext = (char *)dptr;
+        g->arena.ext_size = bytes;
+        g->arena.ext_top = 0;
+        g->arena.budget = bytes;
+    })
+}
+
+int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const uint32_t *nbr,
+                 const uint32_t *w, uint32_t flags) {
+    HYT_GUARD({
+        HYT_REQUIRE(g, HYT_EINVAL, "null handle");
+        HYT_REQUIRE((flags & ~HYT_NO_HUBSORT) == 0, HYT_EINVAL, "unknown flags");
+        load_graph(g, V, E, off, nbr, w, flags);
+    })
+}
+
+int hyt_set_param(hyt_graph *g, const char *key, double v) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && key, HYT_EINVAL, "null argument");
+        Params &p = g->prm;
+        const std::string k(key);
+        auto in = [&](double lo, double hi) {
+            HYT_REQUIRE(v >= lo && v <= hi, HYT_EINVAL, k + " out of range");
+        };
+        auto integral = [&]() { HYT_REQUIRE(v == (double)(int64_t)v, HYT_EINVAL, k + " must be an integer"); };
+        if (k == "alpha") { in(1e-6, 1.0); p.alpha = v; }
+        else if (k == "beta") { in(1e-6, 1.0); p.beta = v; }
+        else if (k == "gamma") { in(1e-6, 1.0); p.gamma = v; }
+        else if (k == "m") { integral(); in(1, 1 << 20); p.m = (uint64_t)v; }
+        else if (k == "mr") { integral(); in(1, 1 << 20); p.mr = (uint64_t)v; }
+        else if (k == "d2") { integral(); in(0, 64); p.d2 = (uint64_t)v; }
+        else if (k == "k") { integral(); in(1, 1024); p.k = (uint64_t)v; }
+        else if (k == "partition_bytes") { integral(); in(16, 1e12); p.partition_bytes = (uint64_t)v; }
+        else if (k == "hub_fraction") { in(0, 1); HYT_REQUIRE(!g->loaded, HYT_ESTATE, "hub_fraction applies at load"); p.hub_fraction = v; }
+        else if (k == "streams") { integral(); in(1, 8); p.streams = (int)v; }
+        else if (k == "engine_mode") { integral(); in(0, 4); p.engine_mode = (int)v; }
+        else if (k == "priority") { integral(); in(-1, 2); p.priority = (int)v; }
+        else if (k == "recompute") { integral(); in(0, 1); p.recompute = (int)v; }
+        else if (k == "damping") { in(1e-6, 1 - 1e-6); p.damping = v; }
+        else if (k == "epsilon") { in(0, 1); p.epsilon = v; }
+        else if (k == "max_iters") { integral(); in(1, 1e9); p.max_iters = (uint64_t)v; }
+        else if (k == "gather_threads") { integral(); in(0, 256); p.gather_threads = (int)v; }
+        else if (k == "compaction_buffer_bytes") { integral(); in(0, 1e12); p.compaction_buffer_bytes = (uint64_t)v; }
+        else if (k == "zc_ctas_per_sm") { integral(); in(1, 32); p.zc_ctas_per_sm = (int)v; }
+        else if (k == "relax_ctas_per_sm") { integral(); in(1, 32); p.relax_ctas_per_sm = (int)v; }
+        else throw Err{HYT_EINVAL, "unknown parameter '" + k + "'"};
+        if (g->loaded) release_run_ctx(g);   // buffers depend on the parameters
+    })
+}
+
+int hyt_run(hyt_graph *g, int algo, uint64_t source) {
+    HYT_GUARD({
+        HYT_REQUIRE(g, HYT_EINVAL, "null handle");
+        run_graph(g, algo, source);
+    })
+}
+
+int hyt_get_values(hyt_graph *g, void *out, uint64_t count) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && out, HYT_EINVAL, "null argument");
+        get_values(g, out, count);
+    })
+}
+
+int hyt_get_stats(hyt_graph *g, hyt_stats *s) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && s, HYT_EINVAL, "null argument");
+        *s = g->stats;
+    })
+}
+
+int hyt_get_iter_log(hyt_graph *g, hyt_iter *rows, uint64_t cap, uint64_t *n) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && n, HYT_EINVAL, "null argument");
+        *n = g->iter_log.size();
+        const uint64_t m = std::min<uint64_t>(cap, g->iter_log.size());
+        if (rows && m) std::memcpy(rows, g->iter_log.data(), m * sizeof(hyt_iter));
+    })
+}
+
+int hyt_get_perm(hyt_graph *g, uint32_t *new_id, uint64_t count) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && new_id, HYT_EINVAL, "null argument");
+        HYT_REQUIRE(g->loaded, HYT_ESTATE, "no graph loaded");
+        HYT_REQUIRE(count == g->V, HYT_EINVAL, "count != V");
+        HYT_CUDA(cudaSetDevice(g->device));
+        HYT_CUDA(cudaMemcpy(new_id, g->new_id_d, g->V * 4, cudaMemcpyDeviceToHost));
+    })
+}
+
+int hyt_debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_parts, uint64_t *bounds,
+                   uint64_t *t, uint64_t *e, uint64_t *a, uint64_t *z, uint8_t *p) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && num_parts, HYT_EINVAL, "null argument");
+        HYT_REQUIRE(active || (!bounds && !t && !p), HYT_EINVAL, "null frontier");
+        debug_plan(g, algo, active, num_parts, bounds, t, e, a, z, p);
+    })
+}
+
+int64_t hyt_combine(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units) {
+    if ((!p && n) || !units || k == 0) { set_error("bad arguments"); return HYT_EINVAL; }
+    return combine_units(p, n, k, units);
+}
+
+int hyt_select_engine(const hyt_graph *g, uint64_t t, uint64_t e, uint64_t a, uint64_t z, uint64_t d1) {
+    if (d1 == 0 || d1 > 64) { set_error("bad d1"); return HYT_EINVAL; }
+    Params def;
+    const Params &p = g ? g->prm : def;
+    return select_engine(t, e, a, z, make_cost(p, (uint32_t)d1));
+}
+
+int hyt_init_dist(hyt_graph *g, int rank, int world, const void *uid) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && uid, HYT_EINVAL, "null argument");
+        HYT_REQUIRE(world >= 1 && rank >= 0 && rank < world, HYT_EINVAL, "bad rank/world");
+        HYT_REQUIRE(!g->loaded, HYT_ESTATE, "call hyt_init_dist before hyt_load_csr");
+        dist_init(g, rank, world, uid);
+    })
+}
+
+void hyt_free(hyt_graph *g) {
+    if (!g) return;
+    try { free_graph(g); } catch (...) {}
+    delete g;
+}
+
+}  // extern "C"

@@ -1,0 +1,841 @@
+// engine.cu -- hyt_run: the per-iteration hybrid-transfer loop.
+//
+// One iteration:
+//   1. plan kernels on the GPU: activity + engine selection per partition
+//      (Alg. 1 L2-12) and the per-engine queues ("pre-combine on GPU");
+//   2. ONE device->host copy of the plan + one sync (Alg. 1 L13);
+//   3. host: task combination into <= k-partition filter units (Alg. 1
+//      L14-24, corrected loop SURVEY C9) and contribution-driven ordering
+//      (hub-driven or delta-driven);
+//   4. multi-stream dispatch: filter units first, in priority
+//      order, each = async bulk copy + relax + one recompute pass;
+//      then the merged zero-copy task (one kernel over Vz); then the
+//      merged compaction task (host gather overlapping the GPU work, bulk copy,
+//      relax over the compacted lists).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <numeric>
+#include <thread>
+#include "graph.h"
+
+namespace hyt {
+
+// ---------------------------------------------------------------------------
+// arena
+// ---------------------------------------------------------------------------
+void *Arena::alloc(uint64_t bytes, const char *what) {
+    bytes = (bytes + 255) & ~255ull;
+    if (budget && used + bytes > budget)
+        throw Err{HYT_ENOMEM, std::string("device budget exceeded allocating ") + what + " (" +
+                                  std::to_string(bytes) + " B; used " + std::to_string(used) + " of " +
+                                  std::to_string(budget) + ")"};
+    void *p = nullptr;
+    uint64_t top_before = ext_top;
+    if (ext) {
+        if (ext_top + bytes > ext_size) throw Err{HYT_ENOMEM, std::string("device arena exhausted: ") + what};
+        p = ext + ext_top;
+        ext_top += bytes;
+    } else {
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw Err{HYT_ENOMEM, std::string("cudaMalloc failed for ") + what + ": " + cudaGetErrorString(e)};
+        }
+    }
+    used += bytes;
+    if (used > peak) peak = used;
+    blocks.push_back({p, bytes, top_before, true});
+    return p;
+}
+
+void Arena::release(void *p) {
+    if (!p) return;
+    for (auto it = blocks.rbegin(); it != blocks.rend(); ++it) {
+        if (it->p == p && it->live) {
+            it->live = false;
+            used -= it->bytes;
+            if (!ext) cudaFree(p);
+            break;
+        }
+    }
+    // pop dead blocks from the top (stack discipline for the external arena)
+    while (!blocks.empty() && !blocks.back().live) {
+        if (ext) ext_top = blocks.back().top_before;
+        blocks.pop_back();
+    }
+}
+
+void Arena::release_all() {
+    for (auto &b : blocks)
+        if (b.live && !ext) cudaFree(b.p);
+    blocks.clear();
+    used = 0;
+    ext_top = 0;
+}
+
+CostParams make_cost(const Params &p, uint32_t d1) {
+    CostParams c;
+    c.d1 = d1; c.d2 = p.d2; c.m = p.m; c.mr = p.mr;
+    const uint64_t den = 1000000;
+    c.an = (uint64_t)(p.alpha * den + 0.5); c.ad = den;
+    c.bn = (uint64_t)(p.beta * den + 0.5); c.bd = den;
+    c.gn = (uint64_t)(p.gamma * den + 0.5); c.gd = den;
+    return c;
+}
+
+// ---------------------------------------------------------------------------
+// host partitioner and task combination
+// ---------------------------------------------------------------------------
+std::vector<uint64_t> partition_bounds(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target) {
+    // greedy sweep (close a partition when the next vertex would exceed target,
+    // unless empty), realised by binary search on the offsets.
+    const uint64_t V = off.size() - 1;
+    std::vector<uint64_t> b{0};
+    uint64_t lo = 0;
+    while (lo < V) {
+        // largest hi with (off[hi] - off[lo]) * d1 <= target, at least lo + 1
+        const uint64_t lim = off[lo] + target / d1;
+        uint64_t hi = std::upper_bound(off.begin() + lo + 1, off.end(), lim) - off.begin() - 1;
+        if (hi <= lo) hi = lo + 1;
+        b.push_back(hi);
+        lo = hi;
+    }
+    return b;
+}
+
+int64_t combine_units(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units) {
+    int64_t nu = 0;
+    uint64_t i = 0;
+    while (i < n) {
+        if (p[i] != ENG_F) { ++i; continue; }
+        const uint64_t start = i;
+        uint64_t len = 0;
+        while (i < n && p[i] == ENG_F && len < k) { ++i; ++len; }
+        units[2 * nu] = start;
+        units[2 * nu + 1] = i;
+        ++nu;
+    }
+    return nu;
+}
+
+// ---------------------------------------------------------------------------
+// host thread pool (compaction gather)
+// ---------------------------------------------------------------------------
+class Pool {
+  public:
+    explicit Pool(unsigned n) {
+        for (unsigned i = 0; i < n; ++i) th_.emplace_back([this, i] { loop(i); });
+    }
+    ~Pool() {
+        { std::lock_guard<std::mutex> l(m_); stop_ = true; }
+        cv_.notify_all();
+        for (auto &t : th_) t.join();
+    }
+    unsigned size() const { return (unsigned)th_.size(); }
+    // run fn(worker) on every worker and wait
+    void run(const std::function<void(unsigned)> &fn) {
+        {
+            std::lock_guard<std::mutex> l(m_);
+            fn_ = fn; pending_ = (unsigned)th_.size(); ++gen_;
+        }
+        cv_.notify_all();
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [this] { return pending_ == 0; });
+    }
+
+  private:
+    void loop(unsigned id) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::function<void(unsigned)> f;
+            {
+                std::unique_lock<std::mutex> l(m_);
+                cv_.wait(l, [&] { return stop_ || gen_ != seen; });
+                if (stop_) return;
+                seen = gen_;
+                f = fn_;
+            }
+            f(id);
+            {
+                std::lock_guard<std::mutex> l(m_);
+                if (--pending_ == 0) done_.notify_all();
+            }
+        }
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_;
+    std::condition_variable cv_, done_;
+    std::function<void(unsigned)> fn_;
+    unsigned pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+// ---------------------------------------------------------------------------
+// run context (cached per handle and edge-record width)
+// ---------------------------------------------------------------------------
+struct EvPair { cudaEvent_t a, b; int tag; };
+enum Tag { TAG_PLAN = 0, TAG_F = 1, TAG_C = 2, TAG_Z = 3, TAG_R = 4, TAG_RECOMP = 5, TAG_COPY = 6 };
+
+struct RunCtx {
+    uint32_t d1 = 0;
+    int algo = -1;
+    uint64_t N = 0, p_lo = 0, p_hi = 0;
+    std::vector<uint64_t> bounds;
+    uint64_t *bounds_d = nullptr, *t_d = nullptr;
+    PartIter *parts_d = nullptr, *parts_h = nullptr;
+    SegHdr *hdr_d = nullptr, *hdr_h = nullptr;
+    QueueBufs q{};
+    uint32_t *val = nullptr, *bm_a = nullptr, *bm_b = nullptr;
+    float *rank = nullptr, *delta = nullptr;
+    int S = 0;
+    std::vector<uint4 *> slot;
+    uint64_t slot_bytes = 0;
+    std::vector<RangeBufs> rb;
+    uint4 *cbuf[2] = {nullptr, nullptr};
+    uint4 *hstage[2] = {nullptr, nullptr};
+    uint64_t cbuf_bytes = 0;
+    uint32_t *cq_v = nullptr;
+    uint64_t *cq_pre = nullptr;
+    uint64_t cq_cap = 0;
+    uint32_t *snap = nullptr;     // multi-GPU: own-range values before the exchange
+    uint64_t *red = nullptr;      // multi-GPU: device scratch for the active-count reduction
+    uint64_t v_lo = 0, v_hi = 0;  // own vertex range
+    std::vector<void *> dev;      // arena blocks (released with the context)
+    std::vector<void *> pinned;   // cudaHostAlloc blocks
+    std::vector<cudaEvent_t> evpool;
+    size_t ev_used = 0;
+    std::vector<EvPair> pending;
+    cudaEvent_t ev_cbuf[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev_done;
+    Pool *pool = nullptr;
+};
+
+static std::mutex g_ctx_mu;
+static std::vector<std::pair<hyt_graph *, RunCtx *>> g_ctx;
+
+static RunCtx *&ctx_of(hyt_graph *g) {
+    std::lock_guard<std::mutex> l(g_ctx_mu);
+    for (auto &x : g_ctx)
+        if (x.first == g) return x.second;
+    g_ctx.push_back({g, nullptr});
+    return g_ctx.back().second;
+}
+
+static void destroy_ctx(hyt_graph *g, RunCtx *c) {
+    if (!c) return;
+    cudaDeviceSynchronize();
+    for (auto e : c->evpool) cudaEventDestroy(e);
+    for (auto e : c->ev_done) cudaEventDestroy(e);
+    for (auto e : c->ev_cbuf) if (e) cudaEventDestroy(e);
+    for (auto it = c->dev.rbegin(); it != c->dev.rend(); ++it) g->arena.release(*it);
+    for (auto p : c->pinned) cudaFreeHost(p);
+    delete c->pool;
+    delete c;
+}
+
+static cudaEvent_t next_event(RunCtx *c) {
+    if (c->ev_used == c->evpool.size()) {
+        cudaEvent_t e;
+        HYT_CUDA(cudaEventCreate(&e));
+        c->evpool.push_back(e);
+    }
+    return c->evpool[c->ev_used++];
+}
+
+static void timed_begin(RunCtx *c, cudaStream_t st, EvPair &ep, int tag) {
+    ep.a = next_event(c); ep.b = next_event(c); ep.tag = tag;
+    HYT_CUDA(cudaEventRecord(ep.a, st));
+}
+static void timed_end(RunCtx *c, cudaStream_t st, EvPair &ep) {
+    HYT_CUDA(cudaEventRecord(ep.b, st));
+    c->pending.push_back(ep);
+}
+
+// Accumulate the timings of completed launches (call after a sync).
+static void harvest(hyt_graph *g, RunCtx *c) {
+    for (auto &ep : c->pending) {
+        float ms = 0;
+        HYT_CUDA(cudaEventElapsedTime(&ms, ep.a, ep.b));
+        EngTime *t = nullptr;
+        switch (ep.tag) {
+            case TAG_PLAN: t = &g->plan_time; break;
+            case TAG_RECOMP: t = &g->recompute_time; break;
+            case TAG_COPY: t = &g->copy_time; break;
+            default: t = &g->eng_time[ep.tag]; break;
+        }
+        t->ms += ms;
+        t->launches += 1;
+    }
+    c->pending.clear();
+    c->ev_used = 0;
+}
+
+template <class T> static T *dalloc(hyt_graph *g, RunCtx *c, uint64_t n, const char *what) {
+    T *p = arena_new<T>(g->arena, n, what);
+    c->dev.push_back(p);
+    return p;
+}
+template <class T> static T *halloc(RunCtx *c, uint64_t n) {
+    void *p = nullptr;
+    HYT_CUDA(cudaHostAlloc(&p, n * sizeof(T) + 64, cudaHostAllocDefault));
+    c->pinned.push_back(p);
+    return (T *)p;
+}
+
+static RunCtx *build_ctx(hyt_graph *g, int algo) {
+    const Params &P = g->prm;
+    RunCtx *c = new RunCtx();
+    try {
+        c->algo = algo;
+        c->d1 = (algo == ALGO_SSSP) ? 8 : 4;
+        const uint64_t V = g->V, W = (V + 31) / 32;
+        c->bounds = partition_bounds(g->off_h, c->d1, P.partition_bytes);
+        c->N = c->bounds.size() - 1;
+        // ---- multi-GPU: contiguous run of partitions with ~equal edge bytes ----
+        c->p_lo = 0; c->p_hi = c->N;
+        if (g->world > 1) {
+            const uint64_t E = g->E;
+            auto cut = [&](int r) -> uint64_t {
+                if (r <= 0) return 0;
+                if (r >= g->world) return c->N;
+                const uint64_t target = E * (uint64_t)r / (uint64_t)g->world;
+                uint64_t i = 0;
+                while (i < c->N && g->off_h[c->bounds[i]] < target) ++i;
+                return i;
+            };
+            c->p_lo = cut(g->rank);
+            c->p_hi = cut(g->rank + 1);
+        }
+        c->v_lo = c->bounds[c->p_lo];
+        c->v_hi = c->bounds[c->p_hi];
+        c->red = dalloc<uint64_t>(g, c, 2, "reduction scratch");
+        if (g->world > 1 && algo != ALGO_PR)
+            c->snap = dalloc<uint32_t>(g, c, c->v_hi - c->v_lo + 1, "exchange snapshot");
+        // ---- vertex state (the paper assumes it fits) ----
+        if (algo == ALGO_PR) {
+            c->rank = dalloc<float>(g, c, V, "rank");
+            c->delta = dalloc<float>(g, c, V, "delta");
+        } else {
+            c->val = dalloc<uint32_t>(g, c, V, "values");
+        }
+        c->bm_a = dalloc<uint32_t>(g, c, W + 1, "frontier");
+        c->bm_b = dalloc<uint32_t>(g, c, W + 1, "next frontier");
+        c->bounds_d = dalloc<uint64_t>(g, c, c->N + 1, "partition bounds");
+        c->t_d = dalloc<uint64_t>(g, c, c->N, "partition edges");
+        c->parts_d = dalloc<PartIter>(g, c, c->N, "partition plan");
+        c->hdr_d = dalloc<SegHdr>(g, c, 1, "segment header");
+        // queue: at most one entry per vertex with out-edges
+        uint64_t vnz = 0, max_part_v = 0;
+        for (uint64_t v = 0; v < V; ++v) vnz += g->off_h[v + 1] > g->off_h[v];
+        c->q.cap = vnz + 1;
+        const uint64_t tot_chunks = chunk_hi(g->E, c->d1) + vnz;
+        c->q.tile_cap = tot_chunks / kTile + 8;
+        c->q.qv = dalloc<uint32_t>(g, c, c->q.cap, "queue vertices");
+        c->q.qpre = dalloc<uint64_t>(g, c, c->q.cap, "queue prefix");
+        c->q.qaux = algo == ALGO_PR ? dalloc<float>(g, c, c->q.cap, "queue contrib") : nullptr;
+        c->q.tile = dalloc<uint32_t>(g, c, c->q.tile_cap, "tile map");
+        // ---- host copies of the plan ----
+        c->parts_h = halloc<PartIter>(c, c->N);
+        c->hdr_h = halloc<SegHdr>(c, 1);
+        std::vector<uint64_t> t(c->N);
+        for (uint64_t i = 0; i < c->N; ++i) t[i] = g->off_h[c->bounds[i + 1]] - g->off_h[c->bounds[i]];
+        HYT_CUDA(cudaMemcpy(c->bounds_d, c->bounds.data(), (c->N + 1) * 8, cudaMemcpyHostToDevice));
+        HYT_CUDA(cudaMemcpy(c->t_d, t.data(), c->N * 8, cudaMemcpyHostToDevice));
+        // ---- staging for filter units: S slots, each holds the largest unit span ----
+        const uint64_t k = std::max<uint64_t>(1, P.k);
+        uint64_t max_span = 0;
+        for (uint64_t i = 0; i < c->N; ++i) {
+            const uint64_t j = std::min(c->N, i + k);
+            const uint64_t c0 = chunk_lo(g->off_h[c->bounds[i]], c->d1);
+            const uint64_t c1 = chunk_hi(g->off_h[c->bounds[j]], c->d1);
+            max_span = std::max(max_span, (c1 - c0) * 16);
+            max_part_v = std::max(max_part_v, c->bounds[j] - c->bounds[i]);
+        }
+        if (P.engine_mode == MODE_RESIDENT) {
+            // edges once into device memory, cached on the handle
+            const int which = c->d1 == 8 ? 1 : 0;
+            if (!g->res_edges[which]) {
+                const uint64_t bytes = chunk_hi(g->E, c->d1) * 16;   // within the 16-B padded store
+                g->res_edges[which] = arena_new<uint4>(g->arena, bytes / 16 + 2, "resident edges");
+                const void *src = which ? (const void *)g->ew_h : (const void *)g->nbr_h;
+                HYT_CUDA(cudaMemcpy(g->res_edges[which], src, bytes, cudaMemcpyHostToDevice));
+            }
+        } else {
+            const uint64_t rq_bytes_per_v = 16 + 4 + (algo == ALGO_PR ? 4 : 0);
+            const uint64_t range_bytes = max_part_v * rq_bytes_per_v + max_span / 16 / kTile * 4 + 4096;
+            const uint64_t cmin = 4ull << 20;
+            int S = std::max(1, std::min(P.streams, 8));
+            while (S > 1 && (uint64_t)S * (max_span + range_bytes) + 2 * cmin > g->arena.avail()) --S;
+            if ((uint64_t)S * (max_span + range_bytes) + 2 * cmin > g->arena.avail())
+                throw Err{HYT_ENOMEM, "device budget too small for one filter staging slot (" +
+                                          std::to_string(max_span) + " B)"};
+            c->S = S;
+            c->slot_bytes = max_span;
+            for (int s = 0; s < S; ++s) {
+                c->slot.push_back(dalloc<uint4>(g, c, max_span / 16 + 2, "filter staging slot"));
+                RangeBufs r{};
+                r.vcap = max_part_v + 64;
+                r.cta_cap = r.vcap / (32 * kRangeWords) + 4;
+                r.q.cap = r.vcap;
+                r.q.tile_cap = max_span / 16 / kTile + 8;
+                r.q.qv = dalloc<uint32_t>(g, c, r.q.cap, "recompute queue");
+                r.q.qpre = dalloc<uint64_t>(g, c, r.q.cap, "recompute prefix");
+                r.q.qaux = algo == ALGO_PR ? dalloc<float>(g, c, r.q.cap, "recompute contrib") : nullptr;
+                r.q.tile = dalloc<uint32_t>(g, c, r.q.tile_cap, "recompute tiles");
+                r.taken = dalloc<uint32_t>(g, c, r.vcap / 32 + 4, "recompute taken");
+                r.scratch = algo == ALGO_PR ? dalloc<float>(g, c, r.vcap, "recompute delta") : nullptr;
+                r.cta_agg = dalloc<uint64_t>(g, c, 2 * r.cta_cap, "recompute aggregates");
+                r.total = dalloc<uint64_t>(g, c, 2, "recompute totals");
+                c->rb.push_back(r);
+            }
+            // compaction double buffer: what is left (capped), at least cmin
+            uint64_t cb = P.compaction_buffer_bytes;
+            if (!cb) {
+                const uint64_t left = g->arena.avail() == UINT64_MAX ? (1ull << 30) : g->arena.avail() / 2;
+                cb = std::min<uint64_t>(256ull << 20, left);
+            }
+            cb = std::max<uint64_t>(cmin, cb) & ~15ull;
+            c->cbuf_bytes = cb;
+            for (int i = 0; i < 2; ++i) {
+                c->cbuf[i] = dalloc<uint4>(g, c, cb / 16, "compaction buffer");
+                c->hstage[i] = halloc<uint4>(c, cb / 16);
+                HYT_CUDA(cudaEventCreateWithFlags(&c->ev_cbuf[i], cudaEventDisableTiming));
+            }
+            c->cq_cap = c->q.cap;
+            c->cq_v = halloc<uint32_t>(c, c->cq_cap);
+            c->cq_pre = halloc<uint64_t>(c, c->cq_cap);
+            unsigned nt = P.gather_threads > 0 ? (unsigned)P.gather_threads
+                                               : std::max(1u, std::thread::hardware_concurrency());
+            c->pool = new Pool(nt);
+        }
+        // streams
+        const int nst = std::max(c->S, 1) + 2;
+        while ((int)g->st.size() < nst) {
+            cudaStream_t s;
+            HYT_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+            g->st.push_back(s);
+        }
+        for (int i = 0; i < nst; ++i) {
+            cudaEvent_t e;
+            HYT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->ev_done.push_back(e);
+        }
+    } catch (...) {
+        destroy_ctx(g, c);
+        throw;
+    }
+    return c;
+}
+
+static RunCtx *get_ctx(hyt_graph *g, int algo) {
+    RunCtx *&c = ctx_of(g);
+    if (c && c->algo == algo) return c;
+    if (c) { destroy_ctx(g, c); c = nullptr; }
+    c = build_ctx(g, algo);
+    return c;
+}
+
+void release_run_ctx(hyt_graph *g) {
+    RunCtx *&c = ctx_of(g);
+    if (c) { destroy_ctx(g, c); c = nullptr; }
+    g->has_result = false;
+}
+
+static DevState make_state(hyt_graph *g, RunCtx *c) {
+    DevState s{};
+    s.V = g->V; s.W = (g->V + 31) / 32;
+    s.off = g->off_d; s.din = g->din_d;
+    s.val = c->val; s.rank = c->rank; s.delta = c->delta;
+    s.bm_cur = c->bm_a; s.bm_next = c->bm_b;
+    s.d1 = c->d1; s.algo = c->algo;
+    s.damping = (float)g->prm.damping;
+    s.epsilon = (float)g->prm.epsilon;
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// compaction gather: chunks [w_lo, w_hi) of the C segment into dst (host)
+// ---------------------------------------------------------------------------
+static void gather_window(RunCtx *c, const uint4 *edges_host, const std::vector<uint64_t> &off, uint64_t n,
+                          uint64_t w_lo, uint64_t w_hi, uint4 *dst) {
+    // first entry covering w_lo
+    const uint64_t *pre = c->cq_pre;
+    uint64_t k0 = std::upper_bound(pre, pre + n, w_lo) - pre - 1;
+    uint64_t k1 = std::lower_bound(pre, pre + n, w_hi) - pre;   // entries [k0, k1)
+    const unsigned nt = c->pool->size();
+    c->pool->run([&](unsigned id) {
+        const uint64_t a = k0 + (k1 - k0) * id / nt, b = k0 + (k1 - k0) * (id + 1) / nt;
+        for (uint64_t k = a; k < b; ++k) {
+            const uint32_t v = c->cq_v[k];
+            const uint64_t c0 = chunk_lo(off[v], c->d1), c1 = chunk_hi(off[v + 1], c->d1);
+            uint64_t lo = pre[k], hi = pre[k] + (c1 - c0);
+            const uint64_t s = std::max(lo, w_lo), e = std::min(hi, w_hi);
+            if (s >= e) continue;
+            std::memcpy(dst + (s - w_lo), edges_host + c0 + (s - lo), (e - s) * 16);
+        }
+    });
+}
+
+static inline double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void run_graph(hyt_graph *g, int algo, uint64_t source) {
+    HYT_REQUIRE(g->loaded, HYT_ESTATE, "no graph loaded");
+    HYT_REQUIRE(algo >= ALGO_BFS && algo <= ALGO_PR, HYT_EINVAL, "unknown algorithm");
+    HYT_REQUIRE(algo == ALGO_CC || algo == ALGO_PR || source < g->V, HYT_EINVAL, "source >= V");
+    HYT_REQUIRE(algo != ALGO_SSSP || g->weighted, HYT_EINVAL, "SSSP needs edge weights");
+    HYT_CUDA(cudaSetDevice(g->device));
+    const Params &P = g->prm;
+    const double t0 = now_ms();
+    RunCtx *c = get_ctx(g, algo);
+    DevState s = make_state(g, c);
+    cudaStream_t main = g->main;
+    const CostParams cp = make_cost(P, c->d1);
+    const int mode = P.engine_mode;
+    const int prio = P.priority >= 0 ? P.priority : (algo == ALGO_PR ? 2 : 1);
+    const int sms = 148;
+    const int relax_ctas = sms * P.relax_ctas_per_sm, zc_ctas = sms * P.zc_ctas_per_sm;
+    const uint4 *edges_host = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
+    const uint4 *edges_mapped = nullptr;
+    HYT_CUDA(cudaHostGetDevicePointer((void **)&edges_mapped, (void *)edges_host, 0));
+    const uint4 *edges_dev = g->res_edges[c->d1 == 8 ? 1 : 0];
+
+    // reset statistics
+    g->stats = hyt_stats{};
+    g->iter_log.clear();
+    for (auto &t : g->eng_time) t = EngTime{};
+    g->recompute_time = g->copy_time = g->plan_time = EngTime{};
+    for (int i = 0; i < ENG_COUNT; ++i) g->eng_chunks[i] = g->eng_edges[i] = 0;
+    g->has_result = false;
+
+    // source in internal ids
+    uint64_t src_int = 0;
+    if (algo == ALGO_BFS || algo == ALGO_SSSP) {
+        uint32_t x = 0;
+        HYT_CUDA(cudaMemcpy(&x, g->new_id_d + source, 4, cudaMemcpyDeviceToHost));
+        src_int = x;
+    }
+    launch_init_values(s, src_int, g->old_of_d, main);
+    HYT_CUDA(cudaGetLastError());
+    if (g->world > 1 && algo == ALGO_PR) {   // only the owner holds a vertex's initial residual
+        if (c->v_lo) HYT_CUDA(cudaMemsetAsync(c->delta, 0, c->v_lo * 4, main));
+        if (c->v_hi < g->V) HYT_CUDA(cudaMemsetAsync(c->delta + c->v_hi, 0, (g->V - c->v_hi) * 4, main));
+    }
+    g->launches = 1;
+
+    const uint64_t np = c->p_hi - c->p_lo;
+    std::vector<uint8_t> pvec(np);
+    std::vector<uint64_t> units(2 * np + 2);
+    const uint64_t max_iters = algo == ALGO_PR ? P.max_iters : UINT64_MAX;
+    uint64_t it = 0;
+    for (; it < max_iters; ++it) {
+        const double ti = now_ms();
+        EvPair ep;
+        timed_begin(c, main, ep, TAG_PLAN);
+        if (algo == ALGO_PR) launch_pr_frontier(s, main);
+        HYT_CUDA(cudaMemsetAsync(c->hdr_d, 0, sizeof(SegHdr), main));
+        launch_plan(s, c->bounds_d, c->t_d, c->p_lo, c->p_hi, mode, cp, c->parts_d, c->hdr_d, main);
+        launch_fill(s, c->bounds_d, c->p_lo, c->p_hi, c->parts_d, c->hdr_d, c->q, main);
+        timed_end(c, main, ep);
+        g->launches += (algo == ALGO_PR) ? 3 : 2;
+        HYT_CUDA(cudaMemcpyAsync(c->parts_h + c->p_lo, c->parts_d + c->p_lo, np * sizeof(PartIter),
+                                 cudaMemcpyDeviceToHost, main));
+        HYT_CUDA(cudaMemcpyAsync(c->hdr_h, c->hdr_d, sizeof(SegHdr), cudaMemcpyDeviceToHost, main));
+        HYT_CUDA(cudaStreamSynchronize(main));
+        HYT_CUDA(cudaGetLastError());
+        harvest(g, c);
+        const SegHdr H = *c->hdr_h;
+        uint64_t active = H.active_vertices;
+        if (g->world > 1) {   // total active vertices over all ranks (termination)
+            HYT_CUDA(cudaMemcpyAsync(c->red, &c->hdr_d->active_vertices, 8, cudaMemcpyDeviceToDevice, main));
+            dist_allreduce_sum_u64(g, c->red, 1, main);
+            uint64_t a2 = 0;
+            HYT_CUDA(cudaMemcpyAsync(&a2, c->red, 8, cudaMemcpyDeviceToHost, main));
+            HYT_CUDA(cudaStreamSynchronize(main));
+            active = a2;
+        }
+        if (active == 0) break;
+
+        hyt_iter row{};
+        row.iteration = it;
+        row.active_vertices = H.active_vertices;
+        row.active_edges = H.active_edges;
+
+        // ---- task combination + ordering (host) ----
+        for (uint64_t i = 0; i < np; ++i) pvec[i] = (uint8_t)c->parts_h[c->p_lo + i].p;
+        const int64_t nu = combine_units(pvec.data(), np, std::max<uint64_t>(1, P.k), units.data());
+        std::vector<uint32_t> order((size_t)nu);
+        std::iota(order.begin(), order.end(), 0u);
+        if (prio != 0 && nu > 1) {
+            std::vector<double> sc((size_t)nu, 0.0);
+            for (int64_t j = 0; j < nu; ++j)
+                for (uint64_t i = units[2 * j]; i < units[2 * j + 1]; ++i) {
+                    const PartIter &pi = c->parts_h[c->p_lo + i];
+                    sc[j] += prio == 2 ? pi.dsum : (double)pi.hub;
+                }
+            std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return sc[x] > sc[y]; });
+        }
+        row.parts_f = (uint32_t)H.parts[ENG_F];
+        row.parts_c = (uint32_t)H.parts[ENG_C];
+        row.parts_z = (uint32_t)H.parts[ENG_Z];
+        row.parts_r = (uint32_t)H.parts[ENG_R];
+        row.units_f = (uint32_t)nu;
+
+        // C queue to the host (needed by the gather) -- enqueued before the GPU work
+        const uint64_t nC = H.ent_count[ENG_C];
+        if (nC) {
+            HYT_CUDA(cudaMemcpyAsync(c->cq_v, c->q.qv + H.ent_base[ENG_C], nC * 4, cudaMemcpyDeviceToHost, main));
+            HYT_CUDA(cudaMemcpyAsync(c->cq_pre, c->q.qpre + H.ent_base[ENG_C], nC * 8, cudaMemcpyDeviceToHost, main));
+        }
+
+        // ---- filter units, in priority order ----
+        const uint64_t fseg_first = H.ent_base[ENG_F], fseg_end = fseg_first + H.ent_count[ENG_F];
+        for (int64_t jj = 0; jj < nu; ++jj) {
+            const uint32_t j = order[jj];
+            const int si = (int)(jj % c->S);
+            cudaStream_t stm = g->st[si];
+            const uint64_t pa = c->p_lo + units[2 * j], pb = c->p_lo + units[2 * j + 1];
+            const uint64_t v_lo = c->bounds[pa], v_hi = c->bounds[pb];
+            const uint64_t s0 = chunk_lo(g->off_h[v_lo], c->d1), s1 = chunk_hi(g->off_h[v_hi], c->d1);
+            const uint64_t bytes = (s1 - s0) * 16;
+            EvPair e1, e2, e3;
+            timed_begin(c, stm, e1, TAG_COPY);
+            HYT_CUDA(cudaMemcpyAsync(c->slot[si], edges_host + s0, bytes, cudaMemcpyHostToDevice, stm));
+            timed_end(c, stm, e1);
+            const uint64_t c_lo = c->parts_h[pa].chunk_base;
+            const uint64_t c_hi = c->parts_h[pb - 1].chunk_base + c->parts_h[pb - 1].chunks;
+            EdgeSrc es{c->slot[si], (int64_t)s0, false};
+            timed_begin(c, stm, e2, TAG_F);
+            launch_relax(s, c->q, H.tile_base[ENG_F], fseg_first, fseg_end, H.chunk_total[ENG_F], c_lo, c_hi,
+                         nullptr, es, relax_ctas, stm);
+            timed_end(c, stm, e2);
+            if (P.recompute) {   // process the loaded unit exactly once more
+                timed_begin(c, stm, e3, TAG_RECOMP);
+                launch_range_queue(s, v_lo, v_hi, c->rb[si], stm);
+                launch_relax(s, c->rb[si].q, 0, 0, 0, 0, 0, 0, c->rb[si].total, es, relax_ctas, stm);
+                timed_end(c, stm, e3);
+            }
+            g->launches += P.recompute ? 4 : 1;
+            row.bytes_f += bytes;
+            g->eng_chunks[ENG_F] += c_hi - c_lo;
+            for (uint64_t i = pa; i < pb; ++i) g->eng_edges[ENG_F] += c->parts_h[i].e;
+        }
+        // ---- merged zero-copy task: one kernel over Vz ----
+        if (H.ent_count[ENG_Z]) {
+            cudaStream_t stm = g->st[c->S];
+            EvPair e1;
+            timed_begin(c, stm, e1, TAG_Z);
+            EdgeSrc es{edges_mapped, 0, false};
+            launch_relax(s, c->q, H.tile_base[ENG_Z], H.ent_base[ENG_Z], H.ent_base[ENG_Z] + H.ent_count[ENG_Z],
+                         H.chunk_total[ENG_Z], 0, H.chunk_total[ENG_Z], nullptr, es, zc_ctas, stm);
+            timed_end(c, stm, e1);
+            g->launches += 1;
+            g->eng_chunks[ENG_Z] += H.chunk_total[ENG_Z];
+        }
+        // ---- resident (build extension) ----
+        if (H.ent_count[ENG_R]) {
+            HYT_REQUIRE(edges_dev != nullptr, HYT_ESTATE, "resident edges missing");
+            cudaStream_t stm = g->st[0];
+            EvPair e1;
+            timed_begin(c, stm, e1, TAG_R);
+            EdgeSrc es{edges_dev, 0, false};
+            launch_relax(s, c->q, H.tile_base[ENG_R], H.ent_base[ENG_R], H.ent_base[ENG_R] + H.ent_count[ENG_R],
+                         H.chunk_total[ENG_R], 0, H.chunk_total[ENG_R], nullptr, es, relax_ctas, stm);
+            timed_end(c, stm, e1);
+            g->launches += 1;
+            g->eng_chunks[ENG_R] += H.chunk_total[ENG_R];
+        }
+        for (uint64_t i = c->p_lo; i < c->p_hi; ++i) {
+            const PartIter &pi = c->parts_h[i];
+            if (pi.p == ENG_Z) { row.bytes_z += pi.z * P.m; g->eng_edges[ENG_Z] += pi.e; }
+            if (pi.p == ENG_C) g->eng_edges[ENG_C] += pi.e;
+            if (pi.p == ENG_R) g->eng_edges[ENG_R] += pi.e;
+        }
+        // ---- merged compaction task: host gather overlapping the GPU work ----
+        if (nC) {
+            HYT_CUDA(cudaStreamSynchronize(main));   // C queue on the host
+            cudaStream_t stm = g->st[c->S + 1];
+            const uint64_t total = H.chunk_total[ENG_C];
+            const uint64_t per = c->cbuf_bytes / 16;
+            uint64_t b = 0;
+            for (uint64_t w_lo = 0; w_lo < total; w_lo += per, ++b) {
+                const uint64_t w_hi = std::min(total, w_lo + per);
+                const int bi = (int)(b & 1);
+                if (b >= 2) HYT_CUDA(cudaEventSynchronize(c->ev_cbuf[bi]));
+                const double tg = now_ms();
+                gather_window(c, edges_host, g->off_h, nC, w_lo, w_hi, c->hstage[bi]);
+                g->stats.gather_ms += now_ms() - tg;
+                EvPair e1, e2;
+                timed_begin(c, stm, e1, TAG_COPY);
+                HYT_CUDA(cudaMemcpyAsync(c->cbuf[bi], c->hstage[bi], (w_hi - w_lo) * 16, cudaMemcpyHostToDevice, stm));
+                timed_end(c, stm, e1);
+                HYT_CUDA(cudaEventRecord(c->ev_cbuf[bi], stm));
+                EdgeSrc es{c->cbuf[bi], 0, true};
+                timed_begin(c, stm, e2, TAG_C);
+                launch_relax(s, c->q, H.tile_base[ENG_C], H.ent_base[ENG_C], H.ent_base[ENG_C] + nC, total, w_lo,
+                             w_hi, nullptr, es, relax_ctas, stm);
+                timed_end(c, stm, e2);
+                g->launches += 1;
+            }
+            row.bytes_c += total * 16;
+            g->eng_chunks[ENG_C] += total;
+        }
+        // ---- join all streams into main ----
+        const int nst = c->S + 2;
+        for (int i = 0; i < nst && i < (int)g->st.size(); ++i) {
+            HYT_CUDA(cudaEventRecord(c->ev_done[i], g->st[i]));
+            HYT_CUDA(cudaStreamWaitEvent(main, c->ev_done[i], 0));
+        }
+        HYT_CUDA(cudaGetLastError());
+        // ---- multi-GPU exchange of pushed values ----
+        if (g->world > 1) {
+            if (algo == ALGO_PR) {
+                // own entries: residual + every rank's pushes; others: outbox -> zero again
+                dist_allreduce_sum_f32(g, c->delta, g->V, main);
+                if (c->v_lo) HYT_CUDA(cudaMemsetAsync(c->delta, 0, c->v_lo * 4, main));
+                if (c->v_hi < g->V) HYT_CUDA(cudaMemsetAsync(c->delta + c->v_hi, 0, (g->V - c->v_hi) * 4, main));
+            } else {
+                HYT_CUDA(cudaMemcpyAsync(c->snap, c->val + c->v_lo, (c->v_hi - c->v_lo) * 4,
+                                         cudaMemcpyDeviceToDevice, main));
+                dist_allreduce_min_u32(g, c->val, g->V, main);
+                launch_mark_improved(c->val, c->snap, c->v_lo, c->v_hi, s.bm_next, main);
+            }
+        }
+        // ---- next frontier ----
+        if (algo != ALGO_PR) {
+            std::swap(s.bm_cur, s.bm_next);
+            std::swap(c->bm_a, c->bm_b);
+            HYT_CUDA(cudaMemsetAsync(s.bm_next, 0, s.W * 4, main));
+        }
+        row.ms = now_ms() - ti;
+        g->stats.bytes_filter += row.bytes_f;
+        g->stats.bytes_compaction += row.bytes_c;
+        g->stats.bytes_zerocopy += row.bytes_z;
+        g->stats.parts_filter += row.parts_f;
+        g->stats.parts_compaction += row.parts_c;
+        g->stats.parts_zerocopy += row.parts_z;
+        g->stats.parts_resident += row.parts_r;
+        g->stats.units_filter += row.units_f;
+        g->stats.edges_relaxed += row.active_edges;
+        g->iter_log.push_back(row);
+    }
+    if (g->world > 1 && algo == ALGO_PR) dist_allreduce_sum_f32(g, c->rank, g->V, main);
+    HYT_CUDA(cudaStreamSynchronize(main));
+    harvest(g, c);
+    const double t1 = now_ms();
+    g->stats.iterations = it;
+    g->stats.time_ns = (uint64_t)((t1 - t0) * 1e6);
+    g->stats.num_partitions = c->N;
+    g->stats.device_bytes_peak = g->arena.peak;
+    double kms = 0;
+    for (int i = 1; i < ENG_COUNT; ++i) kms += g->eng_time[i].ms;
+    g->stats.kernel_ms = kms + g->recompute_time.ms;
+    g->stats.copy_ms = g->copy_time.ms;
+    g->stats.plan_ms = g->plan_time.ms;
+    g->stats.kernel_launches = g->launches;
+    for (int i = 0; i < 8; ++i) { g->stats.eng_ms[i] = 0; g->stats.eng_launches[i] = 0; g->stats.eng_chunks[i] = 0; g->stats.eng_edges[i] = 0; }
+    g->stats.eng_ms[0] = g->plan_time.ms; g->stats.eng_launches[0] = g->plan_time.launches;
+    for (int i = 1; i < ENG_COUNT; ++i) {
+        g->stats.eng_ms[i] = g->eng_time[i].ms; g->stats.eng_launches[i] = g->eng_time[i].launches;
+        g->stats.eng_chunks[i] = g->eng_chunks[i]; g->stats.eng_edges[i] = g->eng_edges[i];
+    }
+    g->stats.eng_ms[5] = g->recompute_time.ms; g->stats.eng_launches[5] = g->recompute_time.launches;
+    g->stats.eng_ms[6] = g->copy_time.ms; g->stats.eng_launches[6] = g->copy_time.launches;
+    g->val_d = c->val; g->rank_d = c->rank; g->delta_d = c->delta;
+    g->last_algo = algo;
+    g->has_result = true;
+}
+
+// ---------------------------------------------------------------------------
+// results
+// ---------------------------------------------------------------------------
+void get_values(hyt_graph *g, void *out, uint64_t count) {
+    HYT_REQUIRE(g->has_result, HYT_ESTATE, "no result: call hyt_run first");
+    HYT_REQUIRE(count == g->V, HYT_EINVAL, "count != V");
+    HYT_CUDA(cudaSetDevice(g->device));
+    RunCtx *c = ctx_of(g);
+    DevState s = make_state(g, c);
+    uint32_t *tmp = arena_new<uint32_t>(g->arena, g->V, "result staging");
+    launch_gather_out(s, g->new_id_d, tmp, g->main);
+    cudaError_t e1 = cudaMemcpyAsync(out, tmp, g->V * 4, cudaMemcpyDeviceToHost, g->main);
+    cudaError_t e2 = cudaStreamSynchronize(g->main);
+    g->arena.release(tmp);
+    HYT_CUDA(e1);
+    HYT_CUDA(e2);
+}
+
+// ---------------------------------------------------------------------------
+// plan parity hook
+// ---------------------------------------------------------------------------
+__global__ void k_active_to_bitmap(const uint8_t *__restrict__ act, const uint32_t *__restrict__ new_id,
+                                   uint64_t V, uint32_t *__restrict__ bm) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < V; u += stride)
+        if (act[u]) {
+            const uint32_t v = new_id[u];
+            atomicOr(&bm[v >> 5], 1u << (v & 31));
+        }
+}
+
+void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_parts, uint64_t *bounds,
+                uint64_t *t, uint64_t *e, uint64_t *a, uint64_t *z, uint8_t *p) {
+    HYT_REQUIRE(g->loaded, HYT_ESTATE, "no graph loaded");
+    HYT_REQUIRE(algo >= ALGO_BFS && algo <= ALGO_PR, HYT_EINVAL, "unknown algorithm");
+    HYT_CUDA(cudaSetDevice(g->device));
+    const uint32_t d1 = algo == ALGO_SSSP ? 8 : 4;
+    std::vector<uint64_t> b = partition_bounds(g->off_h, d1, g->prm.partition_bytes);
+    const uint64_t N = b.size() - 1;
+    *num_parts = N;
+    if (!bounds && !t && !p) return;
+    RunCtx *c = get_ctx(g, algo);
+    DevState s = make_state(g, c);
+    uint8_t *act_d = arena_new<uint8_t>(g->arena, g->V, "debug active");
+    HYT_CUDA(cudaMemcpy(act_d, active, g->V, cudaMemcpyHostToDevice));
+    HYT_CUDA(cudaMemset(s.bm_cur, 0, s.W * 4));
+    k_active_to_bitmap<<<148 * 8, 256, 0, g->main>>>(act_d, g->new_id_d, g->V, s.bm_cur);
+    if (algo == ALGO_PR) {   // the plan kernel reads delta for priorities only
+        HYT_CUDA(cudaMemsetAsync(s.delta, 0, g->V * 4, g->main));
+    }
+    HYT_CUDA(cudaMemsetAsync(c->hdr_d, 0, sizeof(SegHdr), g->main));
+    launch_plan(s, c->bounds_d, c->t_d, 0, N, g->prm.engine_mode, make_cost(g->prm, d1), c->parts_d, c->hdr_d, g->main);
+    std::vector<PartIter> ph(N);
+    HYT_CUDA(cudaMemcpyAsync(ph.data(), c->parts_d, N * sizeof(PartIter), cudaMemcpyDeviceToHost, g->main));
+    HYT_CUDA(cudaStreamSynchronize(g->main));
+    g->arena.release(act_d);
+    for (uint64_t i = 0; i < N; ++i) {
+        if (bounds) bounds[i] = b[i];
+        if (t) t[i] = g->off_h[b[i + 1]] - g->off_h[b[i]];
+        if (e) e[i] = ph[i].e;
+        if (a) a[i] = ph[i].a;
+        if (z) z[i] = ph[i].z;
+        if (p) p[i] = (uint8_t)ph[i].p;
+    }
+    if (bounds) bounds[N] = b[N];
+    g->has_result = false;
+}
+
+void free_graph(hyt_graph *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    release_run_ctx(g);
+    {
+        std::lock_guard<std::mutex> l(g_ctx_mu);
+        for (size_t i = 0; i < g_ctx.size(); ++i)
+            if (g_ctx[i].first == g) { g_ctx.erase(g_ctx.begin() + i); break; }
+    }
+    for (auto s : g->st) cudaStreamDestroy(s);
+    if (g->main) cudaStreamDestroy(g->main);
+    if (g->nbr_h) cudaFreeHost(g->nbr_h);
+    if (g->ew_h) cudaFreeHost(g->ew_h);
+    dist_free(g);
+    g->arena.release_all();
+}
+
+}  // namespace hyt

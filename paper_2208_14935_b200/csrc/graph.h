@@ -1,0 +1,139 @@
+// graph.h -- the handle (struct hyt_graph), the device arena and error plumbing.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+#include "../../include/hyt.h"
+#include "hyt_internal.h"
+
+namespace hyt {
+
+// thread-local last error
+void set_error(const std::string &msg);
+const char *get_error();
+
+struct Err {                       // thrown inside the library, caught at the ABI
+    int code;
+    std::string msg;
+};
+
+#define HYT_CUDA(call)                                                                            \
+    do {                                                                                          \
+        cudaError_t _e = (call);                                                                  \
+        if (_e != cudaSuccess)                                                                    \
+            throw ::hyt::Err{_e == cudaErrorMemoryAllocation ? HYT_ENOMEM : HYT_ECUDA,            \
+                             std::string(#call) + ": " + cudaGetErrorString(_e) + " @" +          \
+                                 __FILE__ + ":" + std::to_string(__LINE__)};                      \
+    } while (0)
+
+#define HYT_REQUIRE(cond, code, msg)                                                              \
+    do {                                                                                          \
+        if (!(cond)) throw ::hyt::Err{(code), (msg)};                                              \
+    } while (0)
+
+// Device arena: every device byte the handle uses goes through here, so the
+// budget is enforced exactly.  Either tracked cudaMalloc blocks or
+// a caller-owned block (e.g. a torch tensor) used as a stack.
+struct Arena {
+    uint64_t budget = 0;       // 0 = no cap
+    uint64_t used = 0, peak = 0;
+    char *ext = nullptr;
+    uint64_t ext_size = 0, ext_top = 0;
+    struct Blk { void *p; uint64_t bytes; uint64_t top_before; bool live; };
+    std::vector<Blk> blocks;
+
+    void *alloc(uint64_t bytes, const char *what);
+    void release(void *p);
+    void release_all();
+    uint64_t avail() const { return budget ? (budget > used ? budget - used : 0) : UINT64_MAX; }
+};
+
+template <class T> T *arena_new(Arena &a, uint64_t n, const char *what) {
+    return (T *)a.alloc(n * sizeof(T) + 16, what);
+}
+
+struct Params {
+    double alpha = 0.8, beta = 0.4, gamma = 0.625;
+    uint64_t m = 128, mr = 256, d2 = 4, k = 4;
+    uint64_t partition_bytes = 32ull << 20;
+    double hub_fraction = 0.08;
+    int streams = 4;
+    int engine_mode = MODE_HYBRID;
+    int priority = -1;
+    int recompute = 1;
+    double damping = 0.85, epsilon = 1e-6;
+    uint64_t max_iters = 1000;
+    int gather_threads = 0;
+    uint64_t compaction_buffer_bytes = 0;
+    int zc_ctas_per_sm = 2;
+    int relax_ctas_per_sm = 4;
+};
+
+CostParams make_cost(const Params &p, uint32_t d1);
+
+// Engine timing accumulator (CUDA events per launch, read after the iteration).
+struct EngTime {
+    double ms = 0;
+    uint64_t launches = 0;
+};
+
+}  // namespace hyt
+
+struct hyt_graph {
+    int device = 0;
+    hyt::Arena arena;
+    hyt::Params prm;
+    // ---- graph (internal, hub-sorted order) ----
+    bool loaded = false;
+    uint64_t V = 0, E = 0;
+    bool weighted = false;
+    uint32_t *nbr_h = nullptr;      // pinned mapped u32[E] (+pad)
+    uint64_t *ew_h = nullptr;       // pinned mapped (id | w<<32) u64[E] (+pad), weighted only
+    std::vector<uint64_t> off_h;    // host copy of offsets u64[V+1]
+    uint64_t *off_d = nullptr;      // device offsets
+    uint32_t *new_id_d = nullptr;   // caller id -> internal id
+    uint32_t *old_of_d = nullptr;   // internal id -> caller id
+    uint32_t *din_d = nullptr;      // in-degree (internal ids)
+    // resident edge cache (engine_mode = resident)
+    uint4 *res_edges[2] = {nullptr, nullptr};   // [0] ids, [1] packed (id,w)
+    // ---- streams ----
+    cudaStream_t main = nullptr;
+    std::vector<cudaStream_t> st;   // worker streams
+    // ---- last run ----
+    int last_algo = -1;
+    bool has_result = false;
+    uint32_t *val_d = nullptr;
+    float *rank_d = nullptr, *delta_d = nullptr;
+    std::vector<void *> run_allocs;  // released at the next run / free
+    hyt_stats stats{};
+    std::vector<hyt_iter> iter_log;
+    hyt::EngTime eng_time[hyt::ENG_COUNT];
+    hyt::EngTime recompute_time, copy_time, plan_time;
+    uint64_t eng_chunks[hyt::ENG_COUNT] = {0, 0, 0, 0, 0};
+    uint64_t eng_edges[hyt::ENG_COUNT] = {0, 0, 0, 0, 0};
+    uint64_t launches = 0;
+    // ---- multi-GPU ----
+    int rank = 0, world = 1;
+    void *nccl_comm = nullptr;
+};
+
+namespace hyt {
+void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const uint32_t *nbr,
+                const uint32_t *w, uint32_t flags);
+void run_graph(hyt_graph *g, int algo, uint64_t source);
+void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_parts, uint64_t *bounds,
+                uint64_t *t, uint64_t *e, uint64_t *a, uint64_t *z, uint8_t *p);
+void get_values(hyt_graph *g, void *out, uint64_t count);
+void free_graph(hyt_graph *g);
+void release_run_ctx(hyt_graph *g);   // drop cached run buffers (parameters changed)
+// host partitioner: greedy 32-MiB sweep by binary search on offsets
+std::vector<uint64_t> partition_bounds(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target);
+int64_t combine_units(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units);
+// multi-GPU exchange (dist.cu)
+void dist_init(hyt_graph *g, int rank, int world, const void *uid);
+void dist_allreduce_min_u32(hyt_graph *g, uint32_t *buf, uint64_t n, cudaStream_t st);
+void dist_allreduce_sum_f32(hyt_graph *g, float *buf, uint64_t n, cudaStream_t st);
+void dist_allreduce_sum_u64(hyt_graph *g, uint64_t *buf, uint64_t n, cudaStream_t st);
+void dist_free(hyt_graph *g);
+}  // namespace hyt

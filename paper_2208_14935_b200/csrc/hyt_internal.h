@@ -1,0 +1,139 @@
+// hyt_internal.h -- internal types shared by the host scheduler and the sm_100a kernels.
+// Nothing here is part of the ABI (include/hyt.h is).
+#pragma once
+#include <cstdint>
+#include <cstddef>
+#include <cuda_runtime.h>
+
+namespace hyt {
+
+// ---------------------------------------------------------------------------
+// Edge storage is addressed in 16-byte CHUNKS (one uint4 load).  A vertex v's
+// edge records occupy bytes [off[v]*d1, off[v+1]*d1) of the edge array; its
+// chunk range is [c0(v), c1(v)) with c0 = off*d1/16 (floor), c1 = ceil.  Every
+// engine processes a queue of active vertices whose exclusive chunk prefix
+// defines a flat chunk space; 8 consecutive lanes read one aligned 128-byte
+// line (the EMOGI "merged and aligned" access).
+// ---------------------------------------------------------------------------
+constexpr int kChunkBytes = 16;
+constexpr int kRelaxThreads = 256;      // threads per relax CTA
+constexpr int kChunksPerThread = 4;     // loads in flight per thread
+constexpr int kTile = kRelaxThreads * kChunksPerThread;   // chunks per tile (16 KiB)
+constexpr int kPlanThreads = 512;       // threads per plan CTA (one CTA per partition)
+constexpr int kRangeWords = 256;        // bitmap words per range-queue CTA
+
+constexpr uint32_t kInf = 0xFFFFFFFFu;
+
+enum Algo : int { ALGO_BFS = 0, ALGO_SSSP = 1, ALGO_CC = 2, ALGO_PR = 3 };
+enum Eng : int { ENG_NONE = 0, ENG_F = 1, ENG_C = 2, ENG_Z = 3, ENG_R = 4, ENG_COUNT = 5 };
+enum Mode : int { MODE_HYBRID = 0, MODE_FILTER = 1, MODE_COMPACTION = 2, MODE_ZEROCOPY = 3, MODE_RESIDENT = 4 };
+
+__host__ __device__ inline uint64_t chunk_lo(uint64_t edge, uint32_t d1) { return (edge * d1) >> 4; }
+__host__ __device__ inline uint64_t chunk_hi(uint64_t edge, uint32_t d1) { return (edge * d1 + 15) >> 4; }
+
+// Exact-integer cost-model constants (rationals for alpha/beta/gamma).
+struct CostParams {
+    uint64_t d1, d2, m, mr;
+    uint64_t an, ad, bn, bd, gn, gd;
+};
+
+// Section 5.1 engine selection, evaluated identically on host (tests) and device.
+// t: partition edges, e: active edges, a: active vertices, z: zero-copy requests.
+__host__ __device__ inline int select_engine(uint64_t t, uint64_t e, uint64_t a, uint64_t z,
+                                             const CostParams &c) {
+    if (e == 0) return ENG_NONE;
+    typedef unsigned __int128 u128;
+    const uint64_t tlp = c.m * c.mr;
+    const uint64_t Tef = (t * c.d1 + tlp - 1) / tlp;                     // Eq. 1
+    const uint64_t Tec = (e * c.d1 + a * c.d2 + tlp - 1) / tlp;          // Eq. 2 (transfer term)
+    const uint64_t nz = (z + c.mr - 1) / c.mr;                            // Eq. 3 TLP count
+    // Tiz = nz * RTT_zc, RTT_zc = gamma + (1-gamma) e/t  ->  nz*(gn t + (gd-gn) e) / (gd t)
+    const u128 num = (u128)nz * ((u128)c.gn * t + (u128)(c.gd - c.gn) * e);
+    const u128 den = (u128)c.gd * t;
+    const bool c1 = (u128)Tec * c.ad < (u128)c.an * Tef;                 // Tec < alpha Tef
+    const bool c2 = (u128)Tec * c.bd * den < (u128)c.bn * num;            // Tec < beta Tiz
+    if (c1 && c2) return ENG_C;
+    if (num < (u128)Tef * den) return ENG_Z;                             // Tiz < Tef
+    return ENG_F;                                                        // ties -> F
+}
+
+// Per-partition, per-iteration aggregates (written by the activity kernel).
+struct PartIter {
+    uint64_t e, a, z;          // active edges / vertices / zero-copy requests (Eq. 1-3 inputs)
+    uint64_t ent, chunks;      // queue entries (active, degree > 0) and their 16-B chunks
+    uint64_t hub;              // sum of D_o*D_i over active vertices (hub priority)
+    uint64_t ent_base, chunk_base;   // offsets inside this partition's engine segment
+    double dsum;               // sum of delta over active vertices (delta priority)
+    uint32_t p, pad;           // engine
+};
+
+// Per-iteration segment header (written by the last activity CTA).
+struct SegHdr {
+    uint64_t ent_base[ENG_COUNT];     // first entry of each engine's segment in the queue
+    uint64_t ent_count[ENG_COUNT];
+    uint64_t chunk_total[ENG_COUNT];
+    uint64_t tile_base[ENG_COUNT];    // first tile-map slot of each segment
+    uint64_t parts[ENG_COUNT];
+    uint64_t active_vertices, active_edges, zc_requests;
+    uint32_t done;                    // CTA completion counter (reset by the last CTA)
+    uint32_t pad;
+};
+
+// Everything a plan / relax kernel needs about the graph and the run state.
+struct DevState {
+    uint64_t V, W;              // vertices, bitmap words
+    const uint64_t *off;        // u64[V+1] (hub-sorted order)
+    const uint32_t *din;        // u32[V] in-degree (hub priority)
+    uint32_t *val;              // u32[V] BFS/SSSP/CC
+    float *rank, *delta;        // f32[V] PR
+    uint32_t *bm_cur, *bm_next; // u32[W]
+    uint32_t d1;
+    int algo;
+    float damping, epsilon;
+};
+
+struct QueueBufs {
+    uint32_t *qv;        // entry -> vertex
+    uint64_t *qpre;      // entry -> exclusive chunk prefix within its segment
+    float *qaux;         // entry -> PR contribution d*delta/D_o
+    uint32_t *tile;      // tile -> first entry whose chunks cover the tile start
+    uint64_t cap, tile_cap;
+};
+
+// Per-stream recompute (range queue) scratch.
+struct RangeBufs {
+    QueueBufs q;
+    uint32_t *taken;     // taken bitmap words of the range
+    float *scratch;      // PR: exchanged delta per vertex of the range
+    uint64_t *cta_agg;   // per-CTA (entries, chunks)
+    uint64_t *total;     // [0] entries, [1] chunks
+    uint64_t vcap, cta_cap;
+};
+
+// ---- kernel launchers (kernels.cu) ----
+void launch_pr_frontier(const DevState &s, cudaStream_t st);
+void launch_plan(const DevState &s, const uint64_t *bounds, const uint64_t *t_static, uint64_t p_lo,
+                 uint64_t p_hi, int mode, const CostParams &cp, PartIter *parts, SegHdr *hdr,
+                 cudaStream_t st);
+void launch_fill(const DevState &s, const uint64_t *bounds, uint64_t p_lo, uint64_t p_hi,
+                 const PartIter *parts, const SegHdr *hdr, QueueBufs q, cudaStream_t st);
+// Edge source for a relax launch.
+struct EdgeSrc {
+    const uint4 *base;   // chunk base pointer (device, staging slot, mapped host, compact buffer)
+    int64_t shift;       // ABS: address = base + (c0(v) + j - shift)
+    bool compact;        // COMPACT: address = base + (c - c_lo)
+};
+// Relax over window [c_lo, c_hi) of the segment whose entries are [seg_first, seg_end)
+// with seg_chunks chunks; dev_tot (range queues) overrides seg_end/seg_chunks/c_hi.
+void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
+                  uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
+                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st);
+void launch_range_queue(const DevState &s, uint64_t v_lo, uint64_t v_hi, RangeBufs r, cudaStream_t st);
+void launch_init_values(const DevState &s, uint64_t src_internal, const uint32_t *old_of, cudaStream_t st);
+void launch_mark_improved(const uint32_t *val, const uint32_t *snap, uint64_t lo, uint64_t hi, uint32_t *bm,
+                          cudaStream_t st);
+void launch_gather_out(const DevState &s, const uint32_t *new_id, void *out_dev, cudaStream_t st);
+
+// ---- load-time kernels (load.cu) ----
+struct LoadOut;
+}  // namespace hyt

@@ -1,0 +1,297 @@
+// load.cu -- hyt_load_csr: CSR validation, hub sorting and the
+// relabelled copy of the edges into library-owned pinned, mapped host memory
+// (the paper's storage split: vertex data on the GPU, edges in host memory,
+// P:75).  All per-vertex and per-edge work runs on the GPU; the
+// caller's edge arrays are read in place through a temporary host mapping.
+#include <cub/cub.cuh>
+#include <algorithm>
+#include <cstring>
+#include <thread>
+#include "graph.h"
+
+namespace hyt {
+
+// ---------------------------------------------------------------------------
+// kernels
+// ---------------------------------------------------------------------------
+__global__ void k_indeg(const uint32_t *__restrict__ nbr, uint64_t E, uint64_t V, uint32_t *__restrict__ din,
+                        uint32_t *__restrict__ bad) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += stride) {
+        const uint32_t x = nbr[i];
+        if (x >= V) { *bad = 1; continue; }
+        atomicAdd(&din[x], 1u);
+    }
+}
+
+// H(v) = D_o D_i / (D_omax D_imax): the denominator is common, so the exact
+// integer key D_o*D_i orders the vertices as H does.
+__global__ void k_hub_keys(const uint64_t *__restrict__ off, const uint32_t *__restrict__ din, uint64_t V,
+                           uint64_t *__restrict__ key, uint32_t *__restrict__ ids) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
+        key[v] = (off[v + 1] - off[v]) * (uint64_t)din[v];
+        ids[v] = (uint32_t)v;
+    }
+}
+
+__global__ void k_mark_hubs(const uint32_t *__restrict__ sorted_ids, uint64_t h, uint32_t *__restrict__ new_id,
+                            uint32_t *__restrict__ nonhub) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < h; i += stride) {
+        const uint32_t v = sorted_ids[i];
+        new_id[v] = (uint32_t)i;      // hubs: 0..h-1 in descending H, ties by id
+        nonhub[v] = 0;
+    }
+}
+
+__global__ void k_fill_u32(uint32_t *p, uint64_t n, uint32_t x) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = x;
+}
+
+// non-hubs keep their natural order after the hubs; build the inverse map and
+// the degree / in-degree arrays in the new order.
+__global__ void k_finish_perm(uint64_t V, uint64_t h, const uint32_t *__restrict__ nonhub,
+                              const uint32_t *__restrict__ nonhub_scan, const uint64_t *__restrict__ off,
+                              const uint32_t *__restrict__ din, uint32_t *__restrict__ new_id,
+                              uint32_t *__restrict__ old_of, uint64_t *__restrict__ deg2,
+                              uint32_t *__restrict__ din2) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
+        uint32_t n;
+        if (nonhub[v]) { n = (uint32_t)(h + nonhub_scan[v]); new_id[v] = n; }
+        else n = new_id[v];
+        old_of[n] = (uint32_t)v;
+        deg2[n] = off[v + 1] - off[v];
+        din2[n] = din[v];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) deg2[V] = 0;
+}
+
+// warp per new row (rows of degree <= big); weights travel with their edge.
+__global__ void k_relabel_rows(uint64_t V, const uint64_t *__restrict__ off_old, const uint64_t *__restrict__ off_new,
+                               const uint32_t *__restrict__ old_of, const uint32_t *__restrict__ new_id,
+                               const uint32_t *__restrict__ nbr_in, const uint32_t *__restrict__ w_in,
+                               uint32_t *__restrict__ nbr_out, uint64_t *__restrict__ ew_out, uint64_t big) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = warp; r < V; r += nwarps) {
+        const uint64_t d = off_new[r], deg = off_new[r + 1] - d;
+        if (deg == 0 || deg > big) continue;
+        const uint64_t s = off_old[old_of[r]];
+        for (uint64_t j = lane; j < deg; j += 32) {
+            const uint32_t y = new_id[nbr_in[s + j]];
+            nbr_out[d + j] = y;
+            if (ew_out) ew_out[d + j] = (uint64_t)y | ((uint64_t)w_in[s + j] << 32);
+        }
+    }
+}
+
+// CTA per (big row, slice) work item.
+__global__ void k_relabel_big(const uint64_t *__restrict__ items, uint64_t slice, const uint64_t *__restrict__ off_old,
+                              const uint64_t *__restrict__ off_new, const uint32_t *__restrict__ old_of,
+                              const uint32_t *__restrict__ new_id, const uint32_t *__restrict__ nbr_in,
+                              const uint32_t *__restrict__ w_in, uint32_t *__restrict__ nbr_out,
+                              uint64_t *__restrict__ ew_out) {
+    const uint64_t r = items[2 * blockIdx.x], sl = items[2 * blockIdx.x + 1];
+    const uint64_t d = off_new[r], deg = off_new[r + 1] - d;
+    const uint64_t s = off_old[old_of[r]];
+    const uint64_t j0 = sl * slice, j1 = min(deg, j0 + slice);
+    for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+        const uint32_t y = new_id[nbr_in[s + j]];
+        nbr_out[d + j] = y;
+        if (ew_out) ew_out[d + j] = (uint64_t)y | ((uint64_t)w_in[s + j] << 32);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+static unsigned grid_for(uint64_t n, int threads = 256, uint64_t cap = 148 * 32) {
+    uint64_t b = (n + threads - 1) / threads;
+    if (b > cap) b = cap;
+    if (b == 0) b = 1;
+    return (unsigned)b;
+}
+
+static void parallel_memcpy(void *dst, const void *src, uint64_t bytes) {
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (bytes < (64ull << 20)) nt = 1;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        uint64_t a = bytes * t / nt, b = bytes * (t + 1) / nt;
+        th.emplace_back([=] { std::memcpy((char *)dst + a, (const char *)src + a, b - a); });
+    }
+    for (auto &x : th) x.join();
+}
+
+// Maps a caller host array for device reads: cudaHostRegister in place, or a
+// temporary pinned copy if registration is refused.
+struct HostView {
+    const void *dev = nullptr;
+    void *reg = nullptr;        // registered base (to unregister)
+    void *tmp = nullptr;        // pinned copy (to free)
+    void open(const void *p, uint64_t bytes) {
+        if (!p || bytes == 0) return;
+        cudaError_t e = cudaHostRegister((void *)p, bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            e = cudaHostRegister((void *)p, bytes, cudaHostRegisterMapped);
+        }
+        if (e == cudaSuccess) {
+            reg = (void *)p;
+        } else {
+            cudaGetLastError();
+            cudaPointerAttributes at{};
+            if (e == cudaErrorHostMemoryAlreadyRegistered &&
+                cudaPointerGetAttributes(&at, p) == cudaSuccess && at.devicePointer) {
+                dev = at.devicePointer;
+                return;
+            }
+            cudaGetLastError();
+            HYT_CUDA(cudaHostAlloc(&tmp, bytes, cudaHostAllocMapped));
+            parallel_memcpy(tmp, p, bytes);
+            void *d = nullptr;
+            HYT_CUDA(cudaHostGetDevicePointer(&d, tmp, 0));
+            dev = d;
+            return;
+        }
+        void *d = nullptr;
+        HYT_CUDA(cudaHostGetDevicePointer(&d, (void *)p, 0));
+        dev = d;
+    }
+    void close() {
+        if (reg) cudaHostUnregister(reg);
+        if (tmp) cudaFreeHost(tmp);
+        reg = tmp = nullptr;
+        dev = nullptr;
+    }
+};
+
+// ---------------------------------------------------------------------------
+// load
+// ---------------------------------------------------------------------------
+void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const uint32_t *nbr,
+                const uint32_t *w, uint32_t flags) {
+    HYT_REQUIRE(!g->loaded, HYT_ESTATE, "graph already loaded");
+    HYT_REQUIRE(V > 0 && V < (1ull << 32), HYT_EINVAL, "V must be in [1, 2^32)");
+    HYT_REQUIRE(off != nullptr && (E == 0 || nbr != nullptr), HYT_EINVAL, "null CSR array");
+    HYT_REQUIRE(off[0] == 0, HYT_EINVAL, "off[0] != 0");
+    HYT_REQUIRE(off[V] == E, HYT_EINVAL, "off[V] != E");
+    for (uint64_t v = 0; v < V; ++v)
+        HYT_REQUIRE(off[v] <= off[v + 1], HYT_EINVAL, "offsets not non-decreasing at " + std::to_string(v));
+    HYT_CUDA(cudaSetDevice(g->device));
+    Arena &A = g->arena;
+    cudaStream_t st = g->main;
+    g->V = V; g->E = E; g->weighted = (w != nullptr);
+
+    // persistent device arrays
+    g->off_d = arena_new<uint64_t>(A, V + 1, "offsets");
+    g->new_id_d = arena_new<uint32_t>(A, V, "new_id");
+    g->old_of_d = arena_new<uint32_t>(A, V, "old_of");
+    g->din_d = arena_new<uint32_t>(A, V, "in_degree");
+
+    // temporaries (released in reverse order)
+    std::vector<void *> tmp;
+    auto T = [&](uint64_t bytes, const char *what) { void *p = A.alloc(bytes, what); tmp.push_back(p); return p; };
+    uint64_t *off_old = (uint64_t *)T((V + 1) * 8, "load: caller offsets");
+    uint32_t *din = (uint32_t *)T(V * 4 + 16, "load: in-degree");
+    uint32_t *bad = (uint32_t *)T(16, "load: flag");
+    uint64_t *deg2 = (uint64_t *)T((V + 1) * 8, "load: degrees");
+    uint32_t *nonhub = (uint32_t *)T(V * 4 + 16, "load: non-hub flags");
+    uint32_t *nonhub_scan = (uint32_t *)T(V * 4 + 16, "load: non-hub scan");
+    HYT_CUDA(cudaMemcpyAsync(off_old, off, (V + 1) * 8, cudaMemcpyHostToDevice, st));
+    HYT_CUDA(cudaMemsetAsync(din, 0, V * 4, st));
+    HYT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+
+    HostView vn, vw;
+    try {
+        vn.open(nbr, E * 4);
+        if (w) vw.open(w, E * 4);
+        if (E) k_indeg<<<grid_for(E), 256, 0, st>>>((const uint32_t *)vn.dev, E, V, din, bad);
+        uint32_t bad_h = 0;
+        HYT_CUDA(cudaMemcpyAsync(&bad_h, bad, 4, cudaMemcpyDeviceToHost, st));
+        HYT_CUDA(cudaStreamSynchronize(st));
+        HYT_REQUIRE(bad_h == 0, HYT_EINVAL, "neighbour id >= V");
+
+        // ---- hub sort: top h = ceil(frac*V) by D_o*D_i ----
+        const uint64_t fden = 1000000;
+        const uint64_t fnum = (uint64_t)(g->prm.hub_fraction * (double)fden + 0.5);
+        uint64_t h = (flags & HYT_NO_HUBSORT) ? 0 : (fnum * V + fden - 1) / fden;
+        if (h > V) h = V;
+        k_fill_u32<<<grid_for(V), 256, 0, st>>>(nonhub, V, 1u);
+        if (h > 0) {
+            uint64_t *key = (uint64_t *)T(V * 8, "load: hub keys");
+            uint64_t *key2 = (uint64_t *)T(V * 8, "load: hub keys sorted");
+            uint32_t *ids = (uint32_t *)T(V * 4 + 16, "load: ids");
+            uint32_t *ids2 = (uint32_t *)T(V * 4 + 16, "load: ids sorted");
+            k_hub_keys<<<grid_for(V), 256, 0, st>>>(off_old, din, V, key, ids);
+            size_t tb = 0;
+            HYT_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, key, key2, ids, ids2, (int)V, 0, 64, st));
+            void *tsort = T(tb + 16, "load: sort temp");
+            HYT_CUDA(cub::DeviceRadixSort::SortPairsDescending(tsort, tb, key, key2, ids, ids2, (int)V, 0, 64, st));
+            k_mark_hubs<<<grid_for(h), 256, 0, st>>>(ids2, h, g->new_id_d, nonhub);
+        }
+        size_t ts = 0;
+        HYT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, ts, nonhub, nonhub_scan, (int)V, st));
+        void *tscan = T(ts + 16, "load: scan temp");
+        HYT_CUDA(cub::DeviceScan::ExclusiveSum(tscan, ts, nonhub, nonhub_scan, (int)V, st));
+        k_finish_perm<<<grid_for(V), 256, 0, st>>>(V, h, nonhub, nonhub_scan, off_old, din, g->new_id_d,
+                                                  g->old_of_d, deg2, g->din_d);
+        size_t t2 = 0;
+        HYT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, deg2, g->off_d, (int)(V + 1), st));
+        void *tscan2 = T(t2 + 16, "load: scan temp 2");
+        HYT_CUDA(cub::DeviceScan::ExclusiveSum(tscan2, t2, deg2, g->off_d, (int)(V + 1), st));
+        g->off_h.resize(V + 1);
+        HYT_CUDA(cudaMemcpyAsync(g->off_h.data(), g->off_d, (V + 1) * 8, cudaMemcpyDeviceToHost, st));
+
+        // ---- pinned mapped edge store (16-B padded so chunk loads never overrun) ----
+        const uint64_t nbytes = ((E * 4 + 15) & ~15ull) + 32;
+        HYT_CUDA(cudaHostAlloc((void **)&g->nbr_h, nbytes, cudaHostAllocMapped | cudaHostAllocPortable));
+        std::memset((char *)g->nbr_h + E * 4, 0, nbytes - E * 4);
+        if (w) {
+            const uint64_t wbytes = ((E * 8 + 15) & ~15ull) + 32;
+            HYT_CUDA(cudaHostAlloc((void **)&g->ew_h, wbytes, cudaHostAllocMapped | cudaHostAllocPortable));
+            std::memset((char *)g->ew_h + E * 8, 0, wbytes - E * 8);
+        }
+        uint32_t *nbr_out = nullptr;
+        uint64_t *ew_out = nullptr;
+        HYT_CUDA(cudaHostGetDevicePointer((void **)&nbr_out, g->nbr_h, 0));
+        if (w) HYT_CUDA(cudaHostGetDevicePointer((void **)&ew_out, g->ew_h, 0));
+        HYT_CUDA(cudaStreamSynchronize(st));   // off_h ready
+
+        const uint64_t big = 8192, slice = 65536;
+        std::vector<uint64_t> items;
+        for (uint64_t r = 0; r < V; ++r) {
+            const uint64_t deg = g->off_h[r + 1] - g->off_h[r];
+            if (deg > big)
+                for (uint64_t sl = 0; sl * slice < deg; ++sl) { items.push_back(r); items.push_back(sl); }
+        }
+        if (E) {
+            k_relabel_rows<<<148 * 16, 256, 0, st>>>(V, off_old, g->off_d, g->old_of_d, g->new_id_d,
+                                                     (const uint32_t *)vn.dev, (const uint32_t *)vw.dev,
+                                                     nbr_out, ew_out, big);
+            if (!items.empty()) {
+                uint64_t *items_d = (uint64_t *)T(items.size() * 8, "load: big rows");
+                HYT_CUDA(cudaMemcpyAsync(items_d, items.data(), items.size() * 8, cudaMemcpyHostToDevice, st));
+                k_relabel_big<<<(unsigned)(items.size() / 2), 512, 0, st>>>(
+                    items_d, slice, off_old, g->off_d, g->old_of_d, g->new_id_d, (const uint32_t *)vn.dev,
+                    (const uint32_t *)vw.dev, nbr_out, ew_out);
+            }
+        }
+        HYT_CUDA(cudaStreamSynchronize(st));
+        HYT_CUDA(cudaGetLastError());
+    } catch (...) {
+        cudaStreamSynchronize(st);
+        vn.close(); vw.close();
+        for (auto it = tmp.rbegin(); it != tmp.rend(); ++it) A.release(*it);
+        throw;
+    }
+    vn.close(); vw.close();
+    for (auto it = tmp.rbegin(); it != tmp.rend(); ++it) A.release(*it);
+    g->loaded = true;
+}
+
+}  // namespace hyt

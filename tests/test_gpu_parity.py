@@ -1,0 +1,294 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Bit-exact for BFS, SSSP (integer weights) and CC; PageRank within
+1e-4 max relative error per vertex (BASELINE.json north_star).  Covers every
+engine mode x partition size {4 KiB, 64 KiB, 32 MiB} x priority, >= 20 RMAT graphs
+(1e3-1e5 vertices) and crafted graphs (empty edge set, isolated vertices, self
+loops, chains, stars, the Fig. 5 toy)."""
+import functools
+
+import numpy as np
+import pytest
+
+import hytgen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+ENGINES = ["hybrid", "filter", "compaction", "zerocopy", "resident"]
+PARTS = [4096, 65536, 32 << 20]
+PR_TOL = 1e-4
+
+
+def rmat_suite():
+    out = []
+    rng = np.random.default_rng(2208)
+    for i in range(20):
+        scale = int(rng.integers(10, 17))
+        V = int(rng.integers(1 << (scale - 1), (1 << scale) + 1))
+        ef = int(rng.integers(4, 24))
+        abc = [(0.57, 0.19, 0.19), (0.45, 0.22, 0.22), (0.25, 0.25, 0.25)][i % 3]
+        sym = i % 4 == 3
+        out.append(dict(name=f"rmat{i}_s{scale}", scale=scale, V=V, E=V * ef // (2 if sym else 1),
+                        abc=abc, seed=100 + i, symmetric=sym))
+    return out
+
+
+RMATS = rmat_suite()
+
+
+@functools.lru_cache(maxsize=None)
+def rmat_graph(i):
+    c = RMATS[i]
+    return hytgen.rmat_csr(c["scale"], c["V"], c["E"], c["abc"], c["seed"], c["symmetric"], weighted=True,
+                           weight_seed=c["seed"] + 7, name=c["name"])
+
+
+def crafted():
+    gs = []
+    gs.append(hytgen.csr_from_edges(5, [], [], weighted=True, name="no_edges"))
+    gs.append(hytgen.csr_from_edges(64, list(range(63)), list(range(1, 64)), weighted=True, name="chain64"))
+    gs.append(hytgen.csr_from_edges(300, [0] * 299 + list(range(1, 300)), list(range(1, 300)) + [0] * 299,
+                                    weighted=True, name="star300"))
+    gs.append(hytgen.csr_from_edges(50, [0, 0, 1, 7, 7, 9, 20, 20], [0, 1, 1, 7, 8, 9, 21, 20], symmetric=True,
+                                    weighted=True, name="selfloops_isolated"))
+    deg = [32, 16, 8, 4, 2, 2, 32, 16, 16]
+    src = [v for v in range(9) for _ in range(deg[v])]
+    dst = [(v + j + 1) % 9 for v in range(9) for j in range(deg[v])]
+    gs.append(hytgen.csr_from_edges(9, src, dst, weighted=True, name="fig5_toy"))
+    # one huge hub (> one 4 KiB partition on its own) plus a long tail
+    V = 20000
+    hub_dst = list(range(1, V))
+    tail_src = list(range(1, V - 1))
+    gs.append(hytgen.csr_from_edges(V, [0] * len(hub_dst) + tail_src, hub_dst + [t + 1 for t in tail_src],
+                                    weighted=True, name="hub_tail"))
+    return gs
+
+
+CRAFTED = crafted()
+
+
+@functools.lru_cache(maxsize=None)
+def expected(gkey, algo):
+    g = gkey_graph(gkey)
+    if algo == "bfs":
+        return oracle.bfs(g.off, g.nbr, src_of(g))
+    if algo == "sssp":
+        return oracle.sssp(g.off, g.nbr, g.w, src_of(g))
+    if algo == "cc":
+        sg = symmetric_version(gkey)
+        return oracle.cc(sg.off, sg.nbr)
+    r, _ = oracle.pr_jacobi(g.off, g.nbr, tol=1e-12)
+    return r
+
+
+def gkey_graph(gkey):
+    kind, i = gkey
+    return rmat_graph(i) if kind == "rmat" else CRAFTED[i]
+
+
+@functools.lru_cache(maxsize=None)
+def symmetric_version(gkey):
+    g = gkey_graph(gkey)
+    if g.symmetric:
+        return g
+    rows = np.repeat(np.arange(g.V), np.diff(g.off.astype(np.int64)))
+    return hytgen.csr_from_edges(g.V, rows, g.nbr, symmetric=True, name=g.name + "_sym")
+
+
+def src_of(g):
+    """vertex 0 if it has out-edges, else the first vertex that does."""
+    deg = np.diff(g.off.astype(np.int64))
+    nz = np.nonzero(deg > 0)[0]
+    return int(nz[0]) if len(nz) and deg[0] == 0 else 0
+
+
+def run_gpu(hyt, g, algo, engine="hybrid", part=32 << 20, prio="auto", budget=0, **kw):
+    G = hyt.Graph(device=0, budget=budget)
+    try:
+        G.load(g.off, g.nbr, g.w)
+        G.set("engine_mode", engine)
+        G.set("partition_bytes", part)
+        G.set("priority", prio)
+        for k, v in kw.items():
+            G.set(k, v)
+        G.run(algo, src_of(g) if algo in ("bfs", "sssp") else 0)
+        return G.values(), G.stats(), G.iter_log()
+    finally:
+        G.close()
+
+
+def assert_pr_close(got, want):
+    rel = np.abs(got.astype(np.float64) - want) / want
+    assert rel.max() <= PR_TOL, f"max rel err {rel.max():.3e} at {rel.argmax()}"
+
+
+ALL_KEYS = [("rmat", i) for i in range(len(RMATS))] + [("crafted", i) for i in range(len(CRAFTED))]
+
+
+@pytest.mark.parametrize("gkey", ALL_KEYS, ids=lambda k: f"{k[0]}{k[1]}")
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+def test_parity_hybrid_default(hyt, gkey, algo):
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    got, st, _ = run_gpu(hyt, g, algo)
+    want = expected(gkey, algo)
+    if algo == "pr":
+        assert_pr_close(got, want)
+    else:
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("part", PARTS)
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+@pytest.mark.parametrize("gi", [0, 4, 9, 13])
+def test_parity_engines_partitions(hyt, engine, part, algo, gi):
+    gkey = ("rmat", gi)
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    got, st, log = run_gpu(hyt, g, algo, engine=engine, part=part)
+    want = expected(gkey, algo)
+    if algo == "pr":
+        assert_pr_close(got, want)
+    else:
+        assert np.array_equal(got, want)
+    if engine == "filter":
+        assert st["parts_compaction"] == 0 and st["parts_zerocopy"] == 0
+    if engine == "zerocopy":
+        assert st["bytes_filter"] == 0 and st["bytes_compaction"] == 0
+
+
+@pytest.mark.parametrize("ci", range(len(CRAFTED)))
+@pytest.mark.parametrize("engine", ENGINES)
+def test_parity_crafted_engines(hyt, ci, engine):
+    gkey = ("crafted", ci)
+    for algo in ("bfs", "sssp", "pr"):
+        g = gkey_graph(gkey)
+        got, _, _ = run_gpu(hyt, g, algo, engine=engine, part=4096)
+        want = expected(gkey, algo)
+        if algo == "pr":
+            assert_pr_close(got, want)
+        else:
+            assert np.array_equal(got, want), (g.name, algo, engine)
+
+
+@pytest.mark.parametrize("prio", ["none", "hub", "delta"])
+@pytest.mark.parametrize("recompute", [0, 1])
+def test_priority_and_recompute(hyt, prio, recompute):
+    gkey = ("rmat", 2)
+    g = gkey_graph(gkey)
+    for algo in ("sssp", "pr"):
+        if prio == "delta" and algo != "pr":
+            continue
+        got, _, _ = run_gpu(hyt, g, algo, part=4096, prio=prio, recompute=recompute)
+        want = expected(gkey, algo)
+        if algo == "pr":
+            assert_pr_close(got, want)
+        else:
+            assert np.array_equal(got, want)
+
+
+def test_hub_sort_permutation_matches_oracle(hyt):
+    for gkey in [("rmat", 1), ("rmat", 5), ("crafted", 2)]:
+        g = gkey_graph(gkey)
+        G = hyt.Graph(device=0)
+        try:
+            G.load(g.off, g.nbr, g.w)
+            assert np.array_equal(G.perm(), oracle.hub_sort(g.off, g.nbr))
+        finally:
+            G.close()
+
+
+@pytest.mark.parametrize("algo,d1", [("bfs", 4), ("sssp", 8)])
+def test_plan_parity(hyt, algo, d1):
+    """the GPU's per-partition aggregates and engine choices equal the
+    oracle's Algorithm 1 on the same frontier snapshot, bit-exact."""
+    for gkey in [("rmat", 3), ("rmat", 8), ("rmat", 12)]:
+        g = gkey_graph(gkey)
+        new_id = oracle.hub_sort(g.off, g.nbr)
+        off2, nbr2, _ = oracle.relabel(g.off, g.nbr, g.w, new_id)
+        rng = np.random.default_rng(7)
+        G = hyt.Graph(device=0)
+        try:
+            G.load(g.off, g.nbr, g.w)
+            for part in (4096, 65536):
+                G.set("partition_bytes", part)
+                for dens in (0.001, 0.02, 0.3, 1.0):
+                    act = (rng.random(g.V) < dens).astype(np.uint8)
+                    gp = G.debug_plan(algo, act)
+                    act2 = np.zeros(g.V, dtype=np.uint8)
+                    act2[new_id] = act
+                    bounds = oracle.partition(off2, d1, part)
+                    assert np.array_equal(gp["bounds"], bounds)
+                    op = oracle.plan(off2, act2, bounds, oracle.CostCfg(d1=d1))
+                    for f in ("t", "e", "a", "z", "p"):
+                        assert np.array_equal(gp[f], getattr(op, f).astype(gp[f].dtype)), (gkey, part, dens, f)
+        finally:
+            G.close()
+
+
+def test_budget_enforced(hyt):
+    g = gkey_graph(("rmat", 6))
+    # state alone does not fit -> HYT_ENOMEM
+    G = hyt.Graph(device=0, budget=4096)
+    try:
+        with pytest.raises(hyt.HytError) as ei:
+            G.load(g.off, g.nbr, g.w)
+        assert ei.value.code == hyt.HYT_ENOMEM
+    finally:
+        G.close()
+    budget = 64 << 20
+    got, st, _ = run_gpu(hyt, g, "sssp", budget=budget, part=65536)
+    assert np.array_equal(got, expected(("rmat", 6), "sssp"))
+    assert 0 < st["device_bytes_peak"] <= budget
+
+
+def test_torch_arena(hyt):
+    g = gkey_graph(("rmat", 7))
+    G = hyt.Graph(device=0, budget=256 << 20, arena="torch")
+    try:
+        G.load(g.off, g.nbr, g.w)
+        G.run("bfs", src_of(g))
+        assert np.array_equal(G.values(), expected(("rmat", 7), "bfs"))
+        assert G.stats()["device_bytes_peak"] <= 256 << 20
+    finally:
+        G.close()
+
+
+def test_r16_config0(hyt):
+    """BASELINE.json configs[0]: RMAT scale-16, BFS + SSSP from vertex 0."""
+    g = hytgen.make("r16", weighted=True)
+    for engine in ("resident", "hybrid"):
+        G = hyt.Graph(device=0)
+        try:
+            G.load(g.off, g.nbr, g.w)
+            G.set("engine_mode", engine)
+            G.run("bfs", 0)
+            assert np.array_equal(G.values(), oracle.bfs(g.off, g.nbr, 0))
+            G.run("sssp", 0)
+            assert np.array_equal(G.values(), oracle.sssp(g.off, g.nbr, g.w, 0))
+        finally:
+            G.close()
+
+
+def test_errors(hyt):
+    g = gkey_graph(("rmat", 0))
+    G = hyt.Graph(device=0)
+    try:
+        with pytest.raises(hyt.HytError) as ei:
+            G.run("bfs", 0)
+        assert ei.value.code == hyt.HYT_ESTATE
+        bad = g.nbr.copy(); bad[3] = g.V + 5
+        with pytest.raises(hyt.HytError) as ei:
+            G.load(g.off, bad, g.w)
+        assert ei.value.code == hyt.HYT_EINVAL
+        G2 = hyt.Graph(device=0)
+        G2.load(g.off, g.nbr, None)
+        with pytest.raises(hyt.HytError) as ei:
+            G2.run("sssp", 0)
+        assert ei.value.code == hyt.HYT_EINVAL
+        with pytest.raises(hyt.HytError):
+            G2.run("bfs", g.V)
+        with pytest.raises(hyt.HytError):
+            G2.set("no_such_key", 1)
+        G2.close()
+    finally:
+        G.close()
