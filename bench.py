@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-shift", type=int, default=6, help="oracle sample = the workload >> cpu_shift")
     ap.add_argument("--json-out", default="")
+    ap.add_argument("--detail-out", default="", help="write per-iteration logs + stats of the last step here")
     return ap.parse_args()
 
 
@@ -295,6 +296,7 @@ def main():
     eng_edges = np.zeros(8, dtype=np.int64)
     link_bytes = 0
     iters = {a: 0 for a in algos}
+    detail = {}
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             barrier()
@@ -313,6 +315,8 @@ def main():
                 eng_edges += np.array(st["eng_edges"])
                 link_bytes += st["bytes_filter"] + st["bytes_compaction"] + st["bytes_zerocopy"]
                 iters[a] = st["iterations"]
+                if args.detail_out:
+                    detail[a] = {"stats": st, "iter_log": G.iter_log()}
             barrier()
             tot = 0.0
             for a, s_ev, e_ev in t_ev:
@@ -426,6 +430,9 @@ def main():
     }
     s = json.dumps(line)
     print(s, flush=True)
+    if args.detail_out:
+        with open(args.detail_out, "w") as f:
+            json.dump({"line": line, "detail": detail}, f)
     if args.json_out:
         with open(args.json_out, "w") as f:
             f.write(s + "\n")

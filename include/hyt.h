@@ -215,6 +215,16 @@ int hyt_select_engine(const hyt_graph *g, uint64_t t, uint64_t e, uint64_t a, ui
 int hyt_nccl_unique_id(void *uid_out_128_bytes);
 int hyt_init_dist(hyt_graph *g, int rank, int world, const void *nccl_uid_128_bytes);
 
+/* The vertex-range split of a multi-GPU job (host routine the library uses,
+ * exposed for CPU tests): with the greedy partitions of `partition_bytes` at
+ * record width d1 over off_host (u64[V+1], the graph as loaded), rank `rank` of
+ * `world` owns partitions [*p_lo, *p_hi) = vertices [*v_lo, *v_hi): contiguous
+ * runs with about E/world edges each (cut where the edge prefix crosses
+ * r*E/world).  Returns the total partition count (>= 0) or HYT_EINVAL.
+ * Needs no GPU. */
+int64_t hyt_rank_range(const uint64_t *off_host, uint64_t V, uint64_t d1, uint64_t partition_bytes, int world,
+                       int rank, uint64_t *p_lo, uint64_t *p_hi, uint64_t *v_lo, uint64_t *v_hi);
+
 /* Release everything (device arena, pinned host memory, streams, NCCL). */
 void hyt_free(hyt_graph *g);
 

@@ -71,6 +71,7 @@ _SIGS = {
     "hyt_combine": ([_vp, _u64, _u64, _vp], ctypes.c_int64),
     "hyt_select_engine": ([_vp, _u64, _u64, _u64, _u64, _u64], _i32),
     "hyt_nccl_unique_id": ([_vp], _i32),
+    "hyt_rank_range": ([_vp, _u64, _u64, _u64, _i32, _i32] + [ctypes.POINTER(_u64)] * 4, ctypes.c_int64),
     "hyt_init_dist": ([_vp, _i32, _i32, _vp], _i32),
     "hyt_free": ([_vp], None),
     "hyt_last_error": ([], ctypes.c_char_p),
@@ -224,6 +225,16 @@ def combine(p, k: int = 4) -> list:
 
 def select_engine(t: int, e: int, a: int, z: int, d1: int) -> int:
     return check(hyt_select_engine(None, t, e, a, z, d1), "hyt_select_engine")
+
+
+def rank_range(off, d1: int, partition_bytes: int, world: int, rank: int) -> dict:
+    """The library's vertex-range split for `rank` of `world` (host only)."""
+    off = np.ascontiguousarray(off, dtype=np.uint64)
+    vals = [_u64() for _ in range(4)]
+    n = check(hyt_rank_range(_ptr(off), len(off) - 1, d1, partition_bytes, world, rank,
+                             *[ctypes.byref(v) for v in vals]), "hyt_rank_range")
+    return {"num_parts": n, "p_lo": vals[0].value, "p_hi": vals[1].value, "v_lo": vals[2].value,
+            "v_hi": vals[3].value}
 
 
 def nccl_unique_id() -> bytes:

@@ -172,6 +172,26 @@ int hyt_select_engine(const hyt_graph *g, uint64_t t, uint64_t e, uint64_t a, ui
     return select_engine(t, e, a, z, make_cost(p, (uint32_t)d1));
 }
 
+int64_t hyt_rank_range(const uint64_t *off, uint64_t V, uint64_t d1, uint64_t partition_bytes, int world, int rank,
+                       uint64_t *p_lo, uint64_t *p_hi, uint64_t *v_lo, uint64_t *v_hi) {
+    if (!off || V == 0 || d1 == 0 || partition_bytes == 0 || world < 1 || rank < 0 || rank >= world || !p_lo ||
+        !p_hi || !v_lo || !v_hi) {
+        set_error("bad arguments");
+        return HYT_EINVAL;
+    }
+    try {
+        std::vector<uint64_t> o(off, off + V + 1);
+        std::vector<uint64_t> b = partition_bounds(o, d1, partition_bytes);
+        rank_partitions(o, b, world, rank, p_lo, p_hi);
+        *v_lo = b[*p_lo];
+        *v_hi = b[*p_hi];
+        return (int64_t)(b.size() - 1);
+    } catch (...) {
+        set_error("internal error");
+        return HYT_EINVAL;
+    }
+}
+
 int hyt_init_dist(hyt_graph *g, int rank, int world, const void *uid) {
     HYT_GUARD({
         HYT_REQUIRE(g && uid, HYT_EINVAL, "null argument");

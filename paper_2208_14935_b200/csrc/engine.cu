@@ -123,6 +123,26 @@ int64_t combine_units(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units)
     return nu;
 }
 
+void rank_partitions(const std::vector<uint64_t> &off, const std::vector<uint64_t> &bounds, int world, int rank,
+                     uint64_t *p_lo, uint64_t *p_hi) {
+    const uint64_t N = bounds.size() - 1, V = off.size() - 1, E = off[V];
+    auto cut = [&](int r) -> uint64_t {
+        if (r <= 0) return 0;
+        if (r >= world) return N;
+        const uint64_t target = (uint64_t)((unsigned __int128)E * (uint64_t)r / (uint64_t)world);
+        // first partition whose starting edge offset reaches the target
+        uint64_t lo = 0, hi = N;
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (off[bounds[mid]] < target) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    *p_lo = cut(rank);
+    *p_hi = cut(rank + 1);
+    if (*p_hi < *p_lo) *p_hi = *p_lo;
+}
+
 // ---------------------------------------------------------------------------
 // host thread pool (compaction gather)
 // ---------------------------------------------------------------------------
@@ -190,6 +210,11 @@ struct RunCtx {
     uint64_t *bounds_d = nullptr, *t_d = nullptr;
     PartIter *parts_d = nullptr, *parts_h = nullptr;
     SegHdr *hdr_d = nullptr, *hdr_h = nullptr;
+    Items items{};                // plan items (device)
+    std::vector<uint64_t> item_first;   // host copy: partition -> first item
+    uint64_t n_items = 0, item_lo = 0, item_hi = 0;
+    ItemAgg *iagg = nullptr;
+    uint64_t *ibase = nullptr;
     QueueBufs q{};
     uint32_t *val = nullptr, *bm_a = nullptr, *bm_b = nullptr;
     float *rank = nullptr, *delta = nullptr;
@@ -298,20 +323,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->bounds = partition_bounds(g->off_h, c->d1, P.partition_bytes);
         c->N = c->bounds.size() - 1;
         // ---- multi-GPU: contiguous run of partitions with ~equal edge bytes ----
-        c->p_lo = 0; c->p_hi = c->N;
-        if (g->world > 1) {
-            const uint64_t E = g->E;
-            auto cut = [&](int r) -> uint64_t {
-                if (r <= 0) return 0;
-                if (r >= g->world) return c->N;
-                const uint64_t target = E * (uint64_t)r / (uint64_t)g->world;
-                uint64_t i = 0;
-                while (i < c->N && g->off_h[c->bounds[i]] < target) ++i;
-                return i;
-            };
-            c->p_lo = cut(g->rank);
-            c->p_hi = cut(g->rank + 1);
-        }
+        rank_partitions(g->off_h, c->bounds, g->world, g->rank, &c->p_lo, &c->p_hi);
         c->v_lo = c->bounds[c->p_lo];
         c->v_hi = c->bounds[c->p_hi];
         c->red = dalloc<uint64_t>(g, c, 2, "reduction scratch");
@@ -330,6 +342,35 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->t_d = dalloc<uint64_t>(g, c, c->N, "partition edges");
         c->parts_d = dalloc<PartIter>(g, c, c->N, "partition plan");
         c->hdr_d = dalloc<SegHdr>(g, c, 1, "segment header");
+        {   // plan items: <= kItemWords words inside one partition (static per run)
+            std::vector<uint32_t> ip;
+            std::vector<uint64_t> iw0, iw1;
+            c->item_first.assign(c->N + 1, 0);
+            for (uint64_t i = 0; i < c->N; ++i) {
+                c->item_first[i] = ip.size();
+                const uint64_t wl = c->bounds[i] >> 5, wh = (c->bounds[i + 1] + 31) >> 5;
+                for (uint64_t w = wl; w < wh; w += kItemWords) {
+                    ip.push_back((uint32_t)i);
+                    iw0.push_back(w);
+                    iw1.push_back(std::min(wh, w + kItemWords));
+                }
+            }
+            c->item_first[c->N] = ip.size();
+            c->n_items = ip.size();
+            c->item_lo = c->item_first[c->p_lo];
+            c->item_hi = c->item_first[c->p_hi];
+            uint32_t *dp = dalloc<uint32_t>(g, c, c->n_items, "item partitions");
+            uint64_t *d0 = dalloc<uint64_t>(g, c, c->n_items, "item words lo");
+            uint64_t *d1w = dalloc<uint64_t>(g, c, c->n_items, "item words hi");
+            uint64_t *df = dalloc<uint64_t>(g, c, c->N + 1, "partition first item");
+            HYT_CUDA(cudaMemcpy(dp, ip.data(), ip.size() * 4, cudaMemcpyHostToDevice));
+            HYT_CUDA(cudaMemcpy(d0, iw0.data(), iw0.size() * 8, cudaMemcpyHostToDevice));
+            HYT_CUDA(cudaMemcpy(d1w, iw1.data(), iw1.size() * 8, cudaMemcpyHostToDevice));
+            HYT_CUDA(cudaMemcpy(df, c->item_first.data(), (c->N + 1) * 8, cudaMemcpyHostToDevice));
+            c->items.part = dp; c->items.w0 = d0; c->items.w1 = d1w; c->items.first = df;
+            c->iagg = dalloc<ItemAgg>(g, c, c->n_items, "item aggregates");
+            c->ibase = dalloc<uint64_t>(g, c, 2 * c->n_items, "item bases");
+        }
         // queue: at most one entry per vertex with out-edges
         uint64_t vnz = 0, max_part_v = 0;
         for (uint64_t v = 0; v < V; ++v) vnz += g->off_h[v + 1] > g->off_h[v];
@@ -368,6 +409,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
             }
         } else {
             const uint64_t rq_bytes_per_v = 16 + 4 + (algo == ALGO_PR ? 4 : 0);
+            (void)rq_bytes_per_v;
             const uint64_t range_bytes = max_part_v * rq_bytes_per_v + max_span / 16 / kTile * 4 + 4096;
             const uint64_t cmin = 4ull << 20;
             int S = std::max(1, std::min(P.streams, 8));
@@ -381,7 +423,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 c->slot.push_back(dalloc<uint4>(g, c, max_span / 16 + 2, "filter staging slot"));
                 RangeBufs r{};
                 r.vcap = max_part_v + 64;
-                r.cta_cap = r.vcap / (32 * kRangeWords) + 4;
+                r.cta_cap = r.vcap / (32 * kItemWords) + 4;
                 r.q.cap = r.vcap;
                 r.q.tile_cap = max_span / 16 / kTile + 8;
                 r.q.qv = dalloc<uint32_t>(g, c, r.q.cap, "recompute queue");
@@ -397,7 +439,8 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
             // compaction double buffer: what is left (capped), at least cmin
             uint64_t cb = P.compaction_buffer_bytes;
             if (!cb) {
-                const uint64_t left = g->arena.avail() == UINT64_MAX ? (1ull << 30) : g->arena.avail() / 2;
+                const uint64_t av = g->arena.avail();
+                const uint64_t left = av == UINT64_MAX ? (1ull << 30) : (av > 8192 ? av / 2 - 4096 : 0);
                 cb = std::min<uint64_t>(256ull << 20, left);
             }
             cb = std::max<uint64_t>(cmin, cb) & ~15ull;
@@ -541,8 +584,10 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         timed_begin(c, main, ep, TAG_PLAN);
         if (algo == ALGO_PR) launch_pr_frontier(s, main);
         HYT_CUDA(cudaMemsetAsync(c->hdr_d, 0, sizeof(SegHdr), main));
-        launch_plan(s, c->bounds_d, c->t_d, c->p_lo, c->p_hi, mode, cp, c->parts_d, c->hdr_d, main);
-        launch_fill(s, c->bounds_d, c->p_lo, c->p_hi, c->parts_d, c->hdr_d, c->q, main);
+        HYT_CUDA(cudaMemsetAsync(c->parts_d + c->p_lo, 0, np * sizeof(PartIter), main));
+        const PlanBufs pb{c->parts_d, c->iagg, c->ibase, c->hdr_d};
+        launch_plan(s, c->bounds_d, c->t_d, c->items, c->item_lo, c->item_hi, c->p_lo, c->p_hi, mode, cp, pb, main);
+        launch_fill(s, c->bounds_d, c->items, c->item_lo, c->item_hi, pb, c->q, main);
         timed_end(c, main, ep);
         g->launches += (algo == ALGO_PR) ? 3 : 2;
         HYT_CUDA(cudaMemcpyAsync(c->parts_h + c->p_lo, c->parts_d + c->p_lo, np * sizeof(PartIter),
@@ -804,7 +849,10 @@ void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_par
         HYT_CUDA(cudaMemsetAsync(s.delta, 0, g->V * 4, g->main));
     }
     HYT_CUDA(cudaMemsetAsync(c->hdr_d, 0, sizeof(SegHdr), g->main));
-    launch_plan(s, c->bounds_d, c->t_d, 0, N, g->prm.engine_mode, make_cost(g->prm, d1), c->parts_d, c->hdr_d, g->main);
+    HYT_CUDA(cudaMemsetAsync(c->parts_d, 0, N * sizeof(PartIter), g->main));
+    const PlanBufs pb{c->parts_d, c->iagg, c->ibase, c->hdr_d};
+    launch_plan(s, c->bounds_d, c->t_d, c->items, 0, c->n_items, 0, N, g->prm.engine_mode, make_cost(g->prm, d1), pb,
+                g->main);
     std::vector<PartIter> ph(N);
     HYT_CUDA(cudaMemcpyAsync(ph.data(), c->parts_d, N * sizeof(PartIter), cudaMemcpyDeviceToHost, g->main));
     HYT_CUDA(cudaStreamSynchronize(g->main));

@@ -130,6 +130,9 @@ void release_run_ctx(hyt_graph *g);   // drop cached run buffers (parameters cha
 // host partitioner: greedy 32-MiB sweep by binary search on offsets
 std::vector<uint64_t> partition_bounds(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target);
 int64_t combine_units(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units);
+// contiguous run of partitions owned by `rank` (about E/world edges each)
+void rank_partitions(const std::vector<uint64_t> &off, const std::vector<uint64_t> &bounds, int world, int rank,
+                     uint64_t *p_lo, uint64_t *p_hi);
 // multi-GPU exchange (dist.cu)
 void dist_init(hyt_graph *g, int rank, int world, const void *uid);
 void dist_allreduce_min_u32(hyt_graph *g, uint32_t *buf, uint64_t n, cudaStream_t st);

@@ -19,8 +19,8 @@ constexpr int kChunkBytes = 16;
 constexpr int kRelaxThreads = 256;      // threads per relax CTA
 constexpr int kChunksPerThread = 4;     // loads in flight per thread
 constexpr int kTile = kRelaxThreads * kChunksPerThread;   // chunks per tile (16 KiB)
-constexpr int kPlanThreads = 512;       // threads per plan CTA (one CTA per partition)
-constexpr int kRangeWords = 256;        // bitmap words per range-queue CTA
+constexpr int kItemWords = 256;         // bitmap words (8192 vertices) per plan item
+constexpr int kItemThreads = 256;       // threads per plan / fill / range CTA
 
 constexpr uint32_t kInf = 0xFFFFFFFFu;
 
@@ -110,13 +110,27 @@ struct RangeBufs {
     uint64_t vcap, cta_cap;
 };
 
-// ---- kernel launchers (kernels.cu) ----
+// Plan items: runs of <= kItemWords bitmap words inside one partition.
+struct Items {
+    const uint32_t *part;     // item -> partition
+    const uint64_t *w0, *w1;  // item word range
+    const uint64_t *first;    // partition -> first item (N+1 entries)
+};
+struct ItemAgg { uint64_t e, a, z, ent, chunks, hub; double dsum; };
+struct PlanBufs {
+    PartIter *parts;          // zeroed before every plan
+    ItemAgg *iagg;
+    uint64_t *ibase;          // item -> (entry base, chunk base) inside its engine segment
+    SegHdr *hdr;              // zeroed before every plan
+};
+
+// ---- kernel launchers (plan.cu, kernels.cu) ----
 void launch_pr_frontier(const DevState &s, cudaStream_t st);
-void launch_plan(const DevState &s, const uint64_t *bounds, const uint64_t *t_static, uint64_t p_lo,
-                 uint64_t p_hi, int mode, const CostParams &cp, PartIter *parts, SegHdr *hdr,
-                 cudaStream_t st);
-void launch_fill(const DevState &s, const uint64_t *bounds, uint64_t p_lo, uint64_t p_hi,
-                 const PartIter *parts, const SegHdr *hdr, QueueBufs q, cudaStream_t st);
+void launch_plan(const DevState &s, const uint64_t *bounds, const uint64_t *t_static, Items it,
+                 uint64_t item_lo, uint64_t item_hi, uint64_t p_lo, uint64_t p_hi, int mode, const CostParams &cp,
+                 PlanBufs pb, cudaStream_t st);
+void launch_fill(const DevState &s, const uint64_t *bounds, Items it, uint64_t item_lo, uint64_t item_hi,
+                 PlanBufs pb, QueueBufs q, cudaStream_t st);
 // Edge source for a relax launch.
 struct EdgeSrc {
     const uint4 *base;   // chunk base pointer (device, staging slot, mapped host, compact buffer)

@@ -1,0 +1,165 @@
+"""Multi-GPU host logic on CPU (world size 2, gloo, 127.0.0.1).
+
+The B200 path shards by vertex range: rank r serves the contiguous run of
+partitions `hyt_rank_range` gives it, pushes into a full-length copy of the
+values, and once per iteration the ranks reduce (min for BFS/SSSP/CC, sum for PR
+deltas), the owners add vertices another rank improved to their next frontier,
+PR zeroes its non-owned delta entries (they are an outbox), and a sum of the
+active counts decides termination (csrc/engine.cu, csrc/dist.cu).
+
+These tests run that exact protocol with torch.distributed/gloo collectives on
+CPU tensors, using the library's own rank split, and check the results against
+the oracle.  The per-rank relax step here is a plain synchronous push (the GPU's
+engines are covered by the -m gpu parity tests)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import hytgen
+import oracle
+import paper_2208_14935_b200 as hyt
+
+INF = 0xFFFFFFFF
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _graph(symmetric=False):
+    return hytgen.rmat_csr(11, 2000, 24000, seed=31, symmetric=symmetric, weighted=True)
+
+
+def _push_min(g, vals, frontier, algo, lo, hi):
+    """one synchronous push from own active vertices into the full-length copy."""
+    new = vals.copy()
+    improved = np.zeros(g.V, dtype=bool)
+    for u in np.nonzero(frontier[lo:hi])[0] + lo:
+        for k in range(int(g.off[u]), int(g.off[u + 1])):
+            v = int(g.nbr[k])
+            cand = vals[u] + (1 if algo == "bfs" else int(g.w[k])) if algo != "cc" else vals[u]
+            if cand < new[v]:
+                new[v] = cand
+                improved[v] = True
+    return new, improved
+
+
+def _worker(rank, world, port, algo, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = _graph(symmetric=(algo == "cc"))
+        rr = hyt.rank_range(g.off, 8 if algo == "sssp" else 4, 4096, world, rank)
+        lo, hi = rr["v_lo"], rr["v_hi"]
+        V = g.V
+        if algo == "pr":
+            d = 0.85
+            rank_v = np.zeros(V)
+            delta = np.zeros(V)
+            delta[lo:hi] = 1 - d                       # only owners hold initial residuals
+            for _ in range(2000):
+                act = np.zeros(V, dtype=bool)
+                act[lo:hi] = delta[lo:hi] > 1e-9
+                n = torch.tensor([int(act.sum())], dtype=torch.int64)
+                dist.all_reduce(n)
+                if n.item() == 0:
+                    break
+                for u in np.nonzero(act)[0]:
+                    du = delta[u]
+                    delta[u] = 0.0
+                    rank_v[u] += du
+                    deg = int(g.off[u + 1] - g.off[u])
+                    for k in range(int(g.off[u]), int(g.off[u + 1])):
+                        delta[int(g.nbr[k])] += d * du / deg
+                t = torch.from_numpy(delta)
+                dist.all_reduce(t)                    # owners: residual + everyone's pushes
+                delta = t.numpy().copy()
+                delta[:lo] = 0.0                      # non-owned entries are an outbox again
+                delta[hi:] = 0.0
+            t = torch.from_numpy(rank_v)
+            dist.all_reduce(t)
+            q.put((rank, rr, t.numpy()))
+            return
+        vals = np.full(V, INF, dtype=np.int64)
+        if algo == "cc":
+            vals = np.arange(V, dtype=np.int64)
+            frontier = np.ones(V, dtype=bool)
+        else:
+            vals[0] = 0
+            frontier = np.zeros(V, dtype=bool)
+            frontier[0] = True
+        for _ in range(10 * V):
+            n = torch.tensor([int(frontier[lo:hi].sum())], dtype=torch.int64)
+            dist.all_reduce(n)
+            if n.item() == 0:
+                break
+            vals, improved = _push_min(g, vals, frontier, algo, lo, hi)
+            snap = vals[lo:hi].copy()
+            t = torch.from_numpy(vals)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            vals = t.numpy().copy()
+            nxt = np.zeros(V, dtype=bool)
+            nxt[lo:hi] = improved[lo:hi] | (vals[lo:hi] < snap)   # owner-side frontier merge
+            frontier = nxt
+        q.put((rank, rr, vals))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(algo, world=2):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, algo, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return sorted(out, key=lambda x: x[0])
+
+
+def test_rank_ranges_tile_and_balance():
+    g = hytgen.rmat_csr(14, 16384, 300000, seed=3)
+    for world in (1, 2, 4, 8):
+        rs = [hyt.rank_range(g.off, 4, 65536, world, r) for r in range(world)]
+        assert rs[0]["p_lo"] == 0 and rs[-1]["p_hi"] == rs[0]["num_parts"]
+        assert rs[0]["v_lo"] == 0 and rs[-1]["v_hi"] == g.V
+        for a, b in zip(rs, rs[1:]):
+            assert a["p_hi"] == b["p_lo"] and a["v_hi"] == b["v_lo"]
+        off = g.off.astype(np.int64)
+        share = [off[r["v_hi"]] - off[r["v_lo"]] for r in rs]
+        # each rank within one partition (+ the largest single vertex) of E/world
+        slack = 65536 // 4 + int(np.diff(off).max())
+        assert max(abs(s - g.E / world) for s in share) <= slack
+
+
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc"])
+def test_gloo_min_exchange_matches_oracle(algo):
+    out = _run(algo)
+    g = _graph(symmetric=(algo == "cc"))
+    want = {"bfs": lambda: oracle.bfs(g.off, g.nbr, 0), "sssp": lambda: oracle.sssp(g.off, g.nbr, g.w, 0),
+            "cc": lambda: oracle.cc(g.off, g.nbr)}[algo]()
+    for rank, rr, vals in out:
+        got = np.where(vals >= INF, INF, vals).astype(np.uint32)
+        assert np.array_equal(got, want), rank
+    assert out[0][1]["v_hi"] == out[1][1]["v_lo"]
+
+
+def test_gloo_pr_outbox_exchange_matches_oracle():
+    out = _run("pr")
+    g = _graph()
+    want, _ = oracle.pr_jacobi(g.off, g.nbr)
+    for rank, rr, r in out:
+        assert np.max(np.abs(r - want) / want) < 1e-7
