@@ -371,26 +371,30 @@ def main():
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
     h2d_peak = measured_h2d_gbs(local)
     tags = hyt.TAGS
-    d1 = {a: 8 if a == "sssp" else 4 for a in algos}
-    kernel_tags = [1, 2, 3, 4, 5]
-    dom = max(kernel_tags, key=lambda i: eng_ms[i]) if eng_ms[kernel_tags].sum() > 0 else 0
-    roof = None
-    if eng_launch[dom] > 0:
-        avg_s = eng_ms[dom] / 1e3 / eng_launch[dom]
-        if dom == 3:    # zero-copy: bound by the host link, algorithmic bytes = touched 128-B lines
-            alg_bytes = eng_chunks[dom] * 16 / eng_launch[dom]
-            roof = {"kernel": "k_relax<zerocopy>", "bound": "pcie", "achieved": alg_bytes / avg_s / 1e9,
-                    "peak": h2d_peak, "unit": "GB/s", "peak_source": "pinned H2D copy measured in this run"}
-        else:           # HBM-side relax: chunk bytes + 4 B destination read per edge
-            alg_bytes = (eng_chunks[dom] * 16 + eng_edges[dom] * 4) / max(1, eng_launch[dom])
-            roof = {"kernel": f"k_relax<{tags[dom]}>", "bound": "hbm", "achieved": alg_bytes / avg_s / 1e9,
-                    "peak": hbm_peak, "unit": "GB/s",
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("fallback") else "")}
-        roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = None
-        roof["avg_launch_ms"] = avg_s * 1e3
-        roof["launches"] = int(eng_launch[dom])
-        roof["share_of_kernel_time"] = float(eng_ms[dom] / max(1e-9, eng_ms[kernel_tags].sum()))
+    kernel_tags = [1, 2, 3, 4, 5]          # relax: filter, compaction, zero-copy, resident, recompute
+
+    def tag_roof(i):
+        if eng_launch[i] == 0:
+            return None
+        avg_s = eng_ms[i] / 1e3 / eng_launch[i]
+        if i == 3:   # zero-copy relax: host-link bound; algorithmic bytes = 16-B chunks read over PCIe
+            alg = eng_chunks[i] * 16 / eng_launch[i]
+            r = {"kernel": "k_relax<zerocopy>", "bound": "pcie", "peak": h2d_peak,
+                 "peak_source": "pinned H2D copy bandwidth measured in this run"}
+        else:        # HBM-side relax: edge chunks + 4-B destination access per edge
+            alg = (eng_chunks[i] * 16 + eng_edges[i] * 4) / eng_launch[i]
+            r = {"kernel": f"k_relax<{tags[i]}>", "bound": "hbm", "peak": hbm_peak,
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" + (" (fallback)" if pk.get("fallback") else "")}
+        r.update({"achieved": alg / avg_s / 1e9, "unit": "GB/s", "bytes_per_launch": alg,
+                  "avg_launch_ms": avg_s * 1e3, "launches": int(eng_launch[i]),
+                  "share_of_kernel_time": float(eng_ms[i] / max(1e-9, eng_ms[kernel_tags].sum()))})
+        r["frac"] = r["achieved"] / r["peak"]
+        r["traffic"] = None
+        return r
+
+    dom = max(kernel_tags, key=lambda i: eng_ms[i])
+    roof = tag_roof(dom)
+    kernels = {tags[i]: tag_roof(i) for i in kernel_tags if eng_launch[i]}
     total_s = sum(times) / 1e3
     host_link = {"bytes": int(link_bytes), "achieved": link_bytes / total_s / 1e9, "peak": h2d_peak,
                  "unit": "GB/s", "frac": link_bytes / total_s / 1e9 / h2d_peak,
@@ -420,6 +424,7 @@ def main():
                    "l2": L2_NOTE, "degree_stats": dstats},
         "per_algo": per_algo,
         "roofline": roof,
+        "kernels": kernels,
         "host_link": host_link,
         "engine_ms": {tags[i]: float(eng_ms[i]) for i in range(7)},
         "cpu_baseline": cpu,

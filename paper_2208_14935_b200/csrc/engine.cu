@@ -230,6 +230,7 @@ struct RunCtx {
     uint64_t cq_cap = 0;
     uint32_t *snap = nullptr;     // multi-GPU: own-range values before the exchange
     uint64_t *red = nullptr;      // multi-GPU: device scratch for the active-count reduction
+    uint64_t *racc = nullptr;     // recompute statistics accumulators (u64[4])
     uint64_t v_lo = 0, v_hi = 0;  // own vertex range
     std::vector<void *> dev;      // arena blocks (released with the context)
     std::vector<void *> pinned;   // cudaHostAlloc blocks
@@ -241,16 +242,7 @@ struct RunCtx {
     Pool *pool = nullptr;
 };
 
-static std::mutex g_ctx_mu;
-static std::vector<std::pair<hyt_graph *, RunCtx *>> g_ctx;
-
-static RunCtx *&ctx_of(hyt_graph *g) {
-    std::lock_guard<std::mutex> l(g_ctx_mu);
-    for (auto &x : g_ctx)
-        if (x.first == g) return x.second;
-    g_ctx.push_back({g, nullptr});
-    return g_ctx.back().second;
-}
+static RunCtx *&ctx_of(hyt_graph *g, int algo) { return *reinterpret_cast<RunCtx **>(&g->ctx[algo]); }
 
 static void destroy_ctx(hyt_graph *g, RunCtx *c) {
     if (!c) return;
@@ -327,6 +319,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->v_lo = c->bounds[c->p_lo];
         c->v_hi = c->bounds[c->p_hi];
         c->red = dalloc<uint64_t>(g, c, 2, "reduction scratch");
+        c->racc = dalloc<uint64_t>(g, c, 4, "recompute statistics");
         if (g->world > 1 && algo != ALGO_PR)
             c->snap = dalloc<uint32_t>(g, c, c->v_hi - c->v_lo + 1, "exchange snapshot");
         // ---- vertex state (the paper assumes it fits) ----
@@ -434,6 +427,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 r.scratch = algo == ALGO_PR ? dalloc<float>(g, c, r.vcap, "recompute delta") : nullptr;
                 r.cta_agg = dalloc<uint64_t>(g, c, 2 * r.cta_cap, "recompute aggregates");
                 r.total = dalloc<uint64_t>(g, c, 2, "recompute totals");
+                r.acc = c->racc;
                 c->rb.push_back(r);
             }
             // compaction double buffer: what is left (capped), at least cmin
@@ -476,17 +470,26 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
     return c;
 }
 
+// One cached context per algorithm; when the budget cannot hold another one,
+// the others are dropped and the build is retried.
 static RunCtx *get_ctx(hyt_graph *g, int algo) {
-    RunCtx *&c = ctx_of(g);
-    if (c && c->algo == algo) return c;
-    if (c) { destroy_ctx(g, c); c = nullptr; }
-    c = build_ctx(g, algo);
+    RunCtx *&c = ctx_of(g, algo);
+    if (c) return c;
+    try {
+        c = build_ctx(g, algo);
+    } catch (const Err &e) {
+        if (e.code != HYT_ENOMEM) throw;
+        for (int a = 0; a < 4; ++a)
+            if (a != algo && ctx_of(g, a)) { destroy_ctx(g, ctx_of(g, a)); ctx_of(g, a) = nullptr; }
+        if (g->last_algo != algo) g->has_result = false;
+        c = build_ctx(g, algo);
+    }
     return c;
 }
 
 void release_run_ctx(hyt_graph *g) {
-    RunCtx *&c = ctx_of(g);
-    if (c) { destroy_ctx(g, c); c = nullptr; }
+    for (int a = 0; a < 4; ++a)
+        if (ctx_of(g, a)) { destroy_ctx(g, ctx_of(g, a)); ctx_of(g, a) = nullptr; }
     g->has_result = false;
 }
 
@@ -657,6 +660,12 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             const uint64_t c_lo = c->parts_h[pa].chunk_base;
             const uint64_t c_hi = c->parts_h[pb - 1].chunk_base + c->parts_h[pb - 1].chunks;
             EdgeSrc es{c->slot[si], (int64_t)s0, false};
+            if (algo == ALGO_PR) {
+                const uint64_t e_lo = fseg_first + c->parts_h[pa].ent_base;
+                const uint64_t e_hi = fseg_first + c->parts_h[pb - 1].ent_base + c->parts_h[pb - 1].ent;
+                launch_take_delta(s, c->q, e_lo, e_hi, stm);
+                g->launches += 1;
+            }
             timed_begin(c, stm, e2, TAG_F);
             launch_relax(s, c->q, H.tile_base[ENG_F], fseg_first, fseg_end, H.chunk_total[ENG_F], c_lo, c_hi,
                          nullptr, es, relax_ctas, stm);
@@ -678,6 +687,10 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             EvPair e1;
             timed_begin(c, stm, e1, TAG_Z);
             EdgeSrc es{edges_mapped, 0, false};
+            if (algo == ALGO_PR) {
+                launch_take_delta(s, c->q, H.ent_base[ENG_Z], H.ent_base[ENG_Z] + H.ent_count[ENG_Z], stm);
+                g->launches += 1;
+            }
             launch_relax(s, c->q, H.tile_base[ENG_Z], H.ent_base[ENG_Z], H.ent_base[ENG_Z] + H.ent_count[ENG_Z],
                          H.chunk_total[ENG_Z], 0, H.chunk_total[ENG_Z], nullptr, es, zc_ctas, stm);
             timed_end(c, stm, e1);
@@ -691,6 +704,10 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             EvPair e1;
             timed_begin(c, stm, e1, TAG_R);
             EdgeSrc es{edges_dev, 0, false};
+            if (algo == ALGO_PR) {
+                launch_take_delta(s, c->q, H.ent_base[ENG_R], H.ent_base[ENG_R] + H.ent_count[ENG_R], stm);
+                g->launches += 1;
+            }
             launch_relax(s, c->q, H.tile_base[ENG_R], H.ent_base[ENG_R], H.ent_base[ENG_R] + H.ent_count[ENG_R],
                          H.chunk_total[ENG_R], 0, H.chunk_total[ENG_R], nullptr, es, relax_ctas, stm);
             timed_end(c, stm, e1);
@@ -709,6 +726,10 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             cudaStream_t stm = g->st[c->S + 1];
             const uint64_t total = H.chunk_total[ENG_C];
             const uint64_t per = c->cbuf_bytes / 16;
+            if (algo == ALGO_PR) {
+                launch_take_delta(s, c->q, H.ent_base[ENG_C], H.ent_base[ENG_C] + nC, stm);
+                g->launches += 1;
+            }
             uint64_t b = 0;
             for (uint64_t w_lo = 0; w_lo < total; w_lo += per, ++b) {
                 const uint64_t w_hi = std::min(total, w_lo + per);
@@ -792,6 +813,12 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         g->stats.eng_chunks[i] = g->eng_chunks[i]; g->stats.eng_edges[i] = g->eng_edges[i];
     }
     g->stats.eng_ms[5] = g->recompute_time.ms; g->stats.eng_launches[5] = g->recompute_time.launches;
+    {
+        uint64_t racc[4] = {0, 0, 0, 0};
+        HYT_CUDA(cudaMemcpy(racc, c->racc, sizeof(racc), cudaMemcpyDeviceToHost));
+        g->stats.eng_chunks[5] = racc[1];
+        g->stats.eng_edges[5] = racc[2];
+    }
     g->stats.eng_ms[6] = g->copy_time.ms; g->stats.eng_launches[6] = g->copy_time.launches;
     g->val_d = c->val; g->rank_d = c->rank; g->delta_d = c->delta;
     g->last_algo = algo;
@@ -805,7 +832,8 @@ void get_values(hyt_graph *g, void *out, uint64_t count) {
     HYT_REQUIRE(g->has_result, HYT_ESTATE, "no result: call hyt_run first");
     HYT_REQUIRE(count == g->V, HYT_EINVAL, "count != V");
     HYT_CUDA(cudaSetDevice(g->device));
-    RunCtx *c = ctx_of(g);
+    RunCtx *c = ctx_of(g, g->last_algo);
+    HYT_REQUIRE(c != nullptr, HYT_ESTATE, "no result: run context was released");
     DevState s = make_state(g, c);
     uint32_t *tmp = arena_new<uint32_t>(g->arena, g->V, "result staging");
     launch_gather_out(s, g->new_id_d, tmp, g->main);
@@ -873,11 +901,6 @@ void free_graph(hyt_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
     release_run_ctx(g);
-    {
-        std::lock_guard<std::mutex> l(g_ctx_mu);
-        for (size_t i = 0; i < g_ctx.size(); ++i)
-            if (g_ctx[i].first == g) { g_ctx.erase(g_ctx.begin() + i); break; }
-    }
     for (auto s : g->st) cudaStreamDestroy(s);
     if (g->main) cudaStreamDestroy(g->main);
     if (g->nbr_h) cudaFreeHost(g->nbr_h);

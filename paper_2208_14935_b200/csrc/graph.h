@@ -113,6 +113,7 @@ struct hyt_graph {
     uint64_t eng_chunks[hyt::ENG_COUNT] = {0, 0, 0, 0, 0};
     uint64_t eng_edges[hyt::ENG_COUNT] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
+    void *ctx[4] = {nullptr, nullptr, nullptr, nullptr};   // cached run contexts, one per algorithm
     // ---- multi-GPU ----
     int rank = 0, world = 1;
     void *nccl_comm = nullptr;

@@ -107,6 +107,7 @@ struct RangeBufs {
     float *scratch;      // PR: exchanged delta per vertex of the range
     uint64_t *cta_agg;   // per-CTA (entries, chunks)
     uint64_t *total;     // [0] entries, [1] chunks
+    uint64_t *acc;       // run statistics: [1] chunks, [2] edges (accumulated)
     uint64_t vcap, cta_cap;
 };
 
@@ -142,6 +143,7 @@ struct EdgeSrc {
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
                   const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st);
+void launch_take_delta(const DevState &s, const QueueBufs &q, uint64_t e_lo, uint64_t e_hi, cudaStream_t st);
 void launch_range_queue(const DevState &s, uint64_t v_lo, uint64_t v_hi, RangeBufs r, cudaStream_t st);
 void launch_init_values(const DevState &s, uint64_t src_internal, const uint32_t *old_of, cudaStream_t st);
 void launch_mark_improved(const uint32_t *val, const uint32_t *snap, uint64_t lo, uint64_t hi, uint32_t *bm,

@@ -188,24 +188,25 @@ __global__ void __launch_bounds__(kItemThreads) k_plan_items(PlanArgs A) {
 // holds word j (already masked).  Pass 1 counts the warp's entries / chunks,
 // pass 2 writes them at base + exclusive position.
 // ---------------------------------------------------------------------------
-struct WarpCount { uint64_t e, c; };
+struct WarpCount { uint64_t e, c, d; };   // entries, chunks, edges
 
 __device__ __forceinline__ WarpCount warp_count(const DevState &s, uint64_t ws, uint32_t myword) {
     const int lane = threadIdx.x & 31;
-    WarpCount r{0, 0};
+    WarpCount r{0, 0, 0};
+    uint64_t c = 0, d = 0;
     for (uint32_t m = __ballot_sync(FULL_MASK, myword != 0); m; m &= m - 1) {
         const int j = __ffs(m) - 1;
         const uint32_t bits = __shfl_sync(FULL_MASK, myword, j);
-        uint64_t nch = 0;
         bool ent = false;
         if ((bits >> lane) & 1u) {
             const uint64_t v = ((ws + j) << 5) + lane;
             const uint64_t o0 = s.off[v], o1 = s.off[v + 1];
-            if (o1 > o0) { ent = true; nch = chunk_hi(o1, s.d1) - chunk_lo(o0, s.d1); }
+            if (o1 > o0) { ent = true; c += chunk_hi(o1, s.d1) - chunk_lo(o0, s.d1); d += o1 - o0; }
         }
         r.e += __popc(__ballot_sync(FULL_MASK, ent));
-        r.c += warp_sum_u64(nch);
     }
+    r.c = warp_sum_u64(c);
+    r.d = warp_sum_u64(d);
     return r;
 }
 
@@ -223,8 +224,12 @@ __device__ __forceinline__ void cta_warp_bases(WarpCount wc, uint64_t *s_e, uint
     *be = xe; *bc = xc; *tot_e = te; *tot_c = tc;
 }
 
-// Pass 2: write the warp's entries.  PR: take delta of every active vertex (deg-0
-// ones are absorbed: rank += delta, nothing pushed).
+// Pass 2: write the warp's entries.  PR in the plan fill (TAKE_DELTA): active
+// vertices without out-edges are absorbed here (rank += delta, nothing pushed,
+// S:457); the others take their delta right before their task runs
+// (launch_take_delta), so a task pushes the mass that arrived earlier in the same
+// iteration (asynchronous processing).  PR in a recompute range queue: the
+// delta taken by k_range_count is in `scratch`.
 template <bool PR, bool TAKE_DELTA>
 __device__ __forceinline__ void warp_write(const DevState &s, uint64_t ws, uint32_t myword, uint64_t base_e,
                                            uint64_t base_c, QueueBufs q, uint64_t tile_base, const float *scratch,
@@ -245,21 +250,13 @@ __device__ __forceinline__ void warp_write(const DevState &s, uint64_t ws, uint3
         const uint32_t b = __ballot_sync(FULL_MASK, ent);
         const uint64_t inc = warp_incl_u64(nch);
         const uint64_t tot = __shfl_sync(FULL_MASK, inc, 31);
-        float dl = 0.0f;
-        if (PR && act) {
-            if (TAKE_DELTA) {
-                dl = atomicExch(&s.delta[v], 0.0f);
-                s.rank[v] += dl;
-            } else {
-                dl = scratch[v - v_lo];
-            }
-        }
+        if (PR && TAKE_DELTA && act && deg == 0) s.rank[v] += atomicExch(&s.delta[v], 0.0f);
         if (ent) {
             const uint64_t idx = run_e + __popc(b & lt);
             const uint64_t pre = run_c + inc - nch;
             q.qv[idx] = (uint32_t)v;
             q.qpre[idx] = pre;
-            if (PR) q.qaux[idx] = s.damping * dl / (float)deg;
+            if (PR && !TAKE_DELTA) q.qaux[idx] = s.damping * scratch[v - v_lo] / (float)deg;
             write_tiles(q.tile + tile_base, pre, nch, (uint32_t)idx);
         }
         run_e += __popc(b);
@@ -388,7 +385,31 @@ __global__ void __launch_bounds__(kItemThreads) k_range_fill(DevState s, uint64_
     uint64_t be, bc, te, tc;
     cta_warp_bases(wc, s_e, s_c, &be, &bc, &te, &tc);
     warp_write<PR, false>(s, ws, myword, pe + be, pc + bc, r.q, 0, r.scratch, v_lo);
+    const uint64_t dsum = block_sum_u64(lane == 0 ? wc.d : 0, sh);
+    if (threadIdx.x == 0 && (tc || dsum)) {   // run statistics of the recompute pass
+        atomicAdd((unsigned long long *)&r.acc[1], (unsigned long long)tc);
+        atomicAdd((unsigned long long *)&r.acc[2], (unsigned long long)dsum);
+    }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) { r.total[0] = pe + te; r.total[1] = pc + tc; }
+}
+
+// PR: take the delta of queue entries [e_lo, e_hi) right before their task runs.
+__global__ void k_take_delta(DevState s, const uint32_t *__restrict__ qv, float *__restrict__ qaux, uint64_t e_lo,
+                             uint64_t e_hi) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = e_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e_hi; k += stride) {
+        const uint32_t v = qv[k];
+        const float dl = atomicExch(&s.delta[v], 0.0f);
+        s.rank[v] += dl;
+        qaux[k] = s.damping * dl / (float)(s.off[(uint64_t)v + 1] - s.off[v]);
+    }
+}
+
+void launch_take_delta(const DevState &s, const QueueBufs &q, uint64_t e_lo, uint64_t e_hi, cudaStream_t st) {
+    if (e_hi <= e_lo) return;
+    uint64_t blocks = (e_hi - e_lo + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_take_delta<<<(unsigned)blocks, 256, 0, st>>>(s, q.qv, q.qaux, e_lo, e_hi);
 }
 
 void launch_range_queue(const DevState &s, uint64_t v_lo, uint64_t v_hi, RangeBufs r, cudaStream_t st) {
