@@ -48,9 +48,17 @@ def _L():
 
 
 def aligned_empty(n: int, dtype, align: int = 4096) -> np.ndarray:
-    """Page-aligned numpy array (so the CUDA side may cudaHostRegister it)."""
+    """Page-aligned numpy array (so the CUDA side may cudaHostRegister it).  Large
+    arrays are private anonymous mappings advised for transparent huge pages, which
+    makes page-locking them ~5x cheaper (tools/pin_bench.cu)."""
+    import mmap
     dtype = np.dtype(dtype)
     nbytes = max(1, n) * dtype.itemsize
+    if nbytes >= (64 << 20) and hasattr(mmap, "MADV_HUGEPAGE"):
+        huge = 2 << 20
+        m = mmap.mmap(-1, (nbytes + huge - 1) // huge * huge, flags=mmap.MAP_PRIVATE | mmap.MAP_ANONYMOUS)
+        m.madvise(mmap.MADV_HUGEPAGE)
+        return np.frombuffer(m, dtype=dtype, count=n)
     raw = np.empty(nbytes + align, dtype=np.uint8)
     off = (-raw.ctypes.data) % align
     return raw[off:off + n * dtype.itemsize].view(dtype)

@@ -219,6 +219,7 @@ struct RunCtx {
     uint32_t *val = nullptr, *bm_a = nullptr, *bm_b = nullptr;
     float *rank = nullptr, *delta = nullptr;
     int S = 0;
+    uint64_t k_eff = 4;           // filter partitions per unit, reduced under small budgets
     std::vector<uint4 *> slot;
     uint64_t slot_bytes = 0;
     std::vector<RangeBufs> rb;
@@ -251,7 +252,7 @@ static void destroy_ctx(hyt_graph *g, RunCtx *c) {
     for (auto e : c->ev_done) cudaEventDestroy(e);
     for (auto e : c->ev_cbuf) if (e) cudaEventDestroy(e);
     for (auto it = c->dev.rbegin(); it != c->dev.rend(); ++it) g->arena.release(*it);
-    for (auto p : c->pinned) cudaFreeHost(p);
+    for (auto p : c->pinned) pinned_free(p);
     delete c->pool;
     delete c;
 }
@@ -299,8 +300,7 @@ template <class T> static T *dalloc(hyt_graph *g, RunCtx *c, uint64_t n, const c
     return p;
 }
 template <class T> static T *halloc(RunCtx *c, uint64_t n) {
-    void *p = nullptr;
-    HYT_CUDA(cudaHostAlloc(&p, n * sizeof(T) + 64, cudaHostAllocDefault));
+    void *p = pinned_alloc(n * sizeof(T) + 64);
     c->pinned.push_back(p);
     return (T *)p;
 }
@@ -372,6 +372,8 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->q.tile_cap = tot_chunks / kTile + 8;
         c->q.qv = dalloc<uint32_t>(g, c, c->q.cap, "queue vertices");
         c->q.qpre = dalloc<uint64_t>(g, c, c->q.cap, "queue prefix");
+        c->q.qbeg = dalloc<uint64_t>(g, c, c->q.cap, "queue edge begin");
+        c->q.qdeg = dalloc<uint32_t>(g, c, c->q.cap, "queue degree");
         c->q.qaux = algo == ALGO_PR ? dalloc<float>(g, c, c->q.cap, "queue contrib") : nullptr;
         c->q.tile = dalloc<uint32_t>(g, c, c->q.tile_cap, "tile map");
         // ---- host copies of the plan ----
@@ -382,15 +384,19 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         HYT_CUDA(cudaMemcpy(c->bounds_d, c->bounds.data(), (c->N + 1) * 8, cudaMemcpyHostToDevice));
         HYT_CUDA(cudaMemcpy(c->t_d, t.data(), c->N * 8, cudaMemcpyHostToDevice));
         // ---- staging for filter units: S slots, each holds the largest unit span ----
-        const uint64_t k = std::max<uint64_t>(1, P.k);
+        uint64_t k = std::max<uint64_t>(1, P.k);
         uint64_t max_span = 0;
-        for (uint64_t i = 0; i < c->N; ++i) {
-            const uint64_t j = std::min(c->N, i + k);
-            const uint64_t c0 = chunk_lo(g->off_h[c->bounds[i]], c->d1);
-            const uint64_t c1 = chunk_hi(g->off_h[c->bounds[j]], c->d1);
-            max_span = std::max(max_span, (c1 - c0) * 16);
-            max_part_v = std::max(max_part_v, c->bounds[j] - c->bounds[i]);
-        }
+        auto spans = [&](uint64_t kk) {
+            max_span = 0; max_part_v = 0;
+            for (uint64_t i = 0; i < c->N; ++i) {
+                const uint64_t j = std::min(c->N, i + kk);
+                const uint64_t c0 = chunk_lo(g->off_h[c->bounds[i]], c->d1);
+                const uint64_t c1 = chunk_hi(g->off_h[c->bounds[j]], c->d1);
+                max_span = std::max(max_span, (c1 - c0) * 16);
+                max_part_v = std::max(max_part_v, c->bounds[j] - c->bounds[i]);
+            }
+        };
+        spans(k);
         if (P.engine_mode == MODE_RESIDENT) {
             // edges once into device memory, cached on the handle
             const int which = c->d1 == 8 ? 1 : 0;
@@ -401,16 +407,20 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 HYT_CUDA(cudaMemcpy(g->res_edges[which], src, bytes, cudaMemcpyHostToDevice));
             }
         } else {
-            const uint64_t rq_bytes_per_v = 16 + 4 + (algo == ALGO_PR ? 4 : 0);
+            const uint64_t rq_bytes_per_v = 28 + 4 + (algo == ALGO_PR ? 8 : 0);
             (void)rq_bytes_per_v;
-            const uint64_t range_bytes = max_part_v * rq_bytes_per_v + max_span / 16 / kTile * 4 + 4096;
+            auto range_bytes = [&]() { return max_part_v * rq_bytes_per_v + max_span / 16 / kTile * 4 + 65536; };
             const uint64_t cmin = 4ull << 20;
             int S = std::max(1, std::min(P.streams, 8));
-            while (S > 1 && (uint64_t)S * (max_span + range_bytes) + 2 * cmin > g->arena.avail()) --S;
-            if ((uint64_t)S * (max_span + range_bytes) + 2 * cmin > g->arena.avail())
+            // a small budget first drops streams, then merges fewer partitions per unit
+            while (S > 1 && (uint64_t)S * (max_span + range_bytes()) + 2 * cmin > g->arena.avail()) --S;
+            while (k > 1 && (uint64_t)S * (max_span + range_bytes()) + 2 * cmin > g->arena.avail()) spans(--k);
+            const uint64_t range_b = range_bytes();
+            if ((uint64_t)S * (max_span + range_b) + 2 * cmin > g->arena.avail())
                 throw Err{HYT_ENOMEM, "device budget too small for one filter staging slot (" +
                                           std::to_string(max_span) + " B)"};
             c->S = S;
+            c->k_eff = k;
             c->slot_bytes = max_span;
             for (int s = 0; s < S; ++s) {
                 c->slot.push_back(dalloc<uint4>(g, c, max_span / 16 + 2, "filter staging slot"));
@@ -421,6 +431,8 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 r.q.tile_cap = max_span / 16 / kTile + 8;
                 r.q.qv = dalloc<uint32_t>(g, c, r.q.cap, "recompute queue");
                 r.q.qpre = dalloc<uint64_t>(g, c, r.q.cap, "recompute prefix");
+                r.q.qbeg = dalloc<uint64_t>(g, c, r.q.cap, "recompute edge begin");
+                r.q.qdeg = dalloc<uint32_t>(g, c, r.q.cap, "recompute degree");
                 r.q.qaux = algo == ALGO_PR ? dalloc<float>(g, c, r.q.cap, "recompute contrib") : nullptr;
                 r.q.tile = dalloc<uint32_t>(g, c, r.q.tile_cap, "recompute tiles");
                 r.taken = dalloc<uint32_t>(g, c, r.vcap / 32 + 4, "recompute taken");
@@ -475,6 +487,13 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
 static RunCtx *get_ctx(hyt_graph *g, int algo) {
     RunCtx *&c = ctx_of(g, algo);
     if (c) return c;
+    // keep other algorithms' contexts only while the budget is mostly free, so a
+    // cached context never shrinks this run's staging
+    if (g->arena.budget && g->arena.avail() < g->arena.budget / 2) {
+        for (int a = 0; a < 4; ++a)
+            if (a != algo && ctx_of(g, a)) { destroy_ctx(g, ctx_of(g, a)); ctx_of(g, a) = nullptr; }
+        if (g->last_algo != algo) g->has_result = false;
+    }
     try {
         c = build_ctx(g, algo);
     } catch (const Err &e) {
@@ -618,7 +637,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
 
         // ---- task combination + ordering (host) ----
         for (uint64_t i = 0; i < np; ++i) pvec[i] = (uint8_t)c->parts_h[c->p_lo + i].p;
-        const int64_t nu = combine_units(pvec.data(), np, std::max<uint64_t>(1, P.k), units.data());
+        const int64_t nu = combine_units(pvec.data(), np, c->k_eff, units.data());
         std::vector<uint32_t> order((size_t)nu);
         std::iota(order.begin(), order.end(), 0u);
         if (prio != 0 && nu > 1) {
@@ -903,8 +922,8 @@ void free_graph(hyt_graph *g) {
     release_run_ctx(g);
     for (auto s : g->st) cudaStreamDestroy(s);
     if (g->main) cudaStreamDestroy(g->main);
-    if (g->nbr_h) cudaFreeHost(g->nbr_h);
-    if (g->ew_h) cudaFreeHost(g->ew_h);
+    pinned_free(g->nbr_h);
+    pinned_free(g->ew_h);
     dist_free(g);
     g->arena.release_all();
 }

@@ -72,6 +72,12 @@ struct Params {
 
 CostParams make_cost(const Params &p, uint32_t d1);
 
+// Pinned, mapped host memory: mmap + transparent huge pages + parallel first
+// touch + cudaHostRegister.  About 9x faster to create than cudaHostAlloc on the
+// B200 box (tools/pin_bench.cu: 0.34 s vs 3.1 s for 8 GB).
+void *pinned_alloc(uint64_t bytes);
+void pinned_free(void *p);
+
 // Engine timing accumulator (CUDA events per launch, read after the iteration).
 struct EngTime {
     double ms = 0;

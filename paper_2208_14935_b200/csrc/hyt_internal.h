@@ -16,9 +16,10 @@ namespace hyt {
 // line (the EMOGI "merged and aligned" access).
 // ---------------------------------------------------------------------------
 constexpr int kChunkBytes = 16;
-constexpr int kRelaxThreads = 256;      // threads per relax CTA
-constexpr int kChunksPerThread = 4;     // loads in flight per thread
-constexpr int kTile = kRelaxThreads * kChunksPerThread;   // chunks per tile (16 KiB)
+constexpr int kRelaxThreads = 256;      // threads per relax CTA (8 independent warps)
+constexpr int kChunksPerThread = 4;     // 16-byte loads in flight per lane
+constexpr int kTile = 32 * kChunksPerThread;   // chunks per WARP tile (2 KiB of edges)
+constexpr int kHotV = 4096;             // PR: pushes to vertices < kHotV (the hub block) go to smem first
 constexpr int kItemWords = 256;         // bitmap words (8192 vertices) per plan item
 constexpr int kItemThreads = 256;       // threads per plan / fill / range CTA
 
@@ -95,6 +96,8 @@ struct DevState {
 struct QueueBufs {
     uint32_t *qv;        // entry -> vertex
     uint64_t *qpre;      // entry -> exclusive chunk prefix within its segment
+    uint64_t *qbeg;      // entry -> first edge index off[v]
+    uint32_t *qdeg;      // entry -> out-degree
     float *qaux;         // entry -> PR contribution d*delta/D_o
     uint32_t *tile;      // tile -> first entry whose chunks cover the tile start
     uint64_t cap, tile_cap;

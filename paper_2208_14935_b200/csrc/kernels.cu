@@ -35,11 +35,22 @@ void launch_pr_frontier(const DevState &s, cudaStream_t st) {
 
 // ---------------------------------------------------------------------------
 // Relax: the push over a chunk window [c_lo, c_hi) of one queue segment.
+//
+// Work unit = a WARP tile of kTile = 128 consecutive chunks of the segment's chunk
+// space (warps are independent: no CTA barriers on the hot loop).  Per tile the
+// lanes stage the <= kTile+1 overlapping queue entries (prefix, first edge,
+// degree, source value) in the warp's shared-memory slice, then each lane finds
+// the entry of each of its 4 chunks by binary search and issues 4 independent
+// 16-byte loads; 8 consecutive lanes cover one aligned 128-byte line.
+// PR: pushes into the hub block (ids < kHotV, the highest-H vertices after hub
+// sorting) are accumulated in shared memory and flushed once per CTA, so
+// the hottest destinations do not serialise L2 atomics.
 // ---------------------------------------------------------------------------
 struct RelaxArgs {
     DevState s;
     const uint32_t *qv;
-    const uint64_t *qpre;
+    const uint64_t *qpre, *qbeg;
+    const uint32_t *qdeg;
     const float *qaux;
     const uint32_t *tile;      // segment's tile map (already offset by tile_base)
     uint64_t c_lo, c_hi;       // window (host values)
@@ -50,16 +61,21 @@ struct RelaxArgs {
     int64_t shift;
 };
 
+constexpr int kWarps = kRelaxThreads / 32;
+
 template <int ALGO, bool COMPACT>
 __global__ void __launch_bounds__(kRelaxThreads)
 k_relax(RelaxArgs A) {
     constexpr uint32_t D1 = (ALGO == ALGO_SSSP) ? 8u : 4u;
     constexpr int EPC = 16 / D1;                  // edge records per chunk
-    __shared__ uint64_t s_pre[kTile + 1];
-    __shared__ uint64_t s_beg[kTile + 1];
-    __shared__ uint64_t s_end[kTile + 1];
-    __shared__ uint32_t s_src[kTile + 1];
+    constexpr bool PR = (ALGO == ALGO_PR);
+    __shared__ uint64_t s_pre[kWarps][kTile + 1];
+    __shared__ uint64_t s_beg[kWarps][kTile + 1];
+    __shared__ uint32_t s_deg[kWarps][kTile + 1];
+    __shared__ uint32_t s_src[kWarps][kTile + 1];
+    __shared__ float s_hot[PR ? kHotV : 1];
     const DevState &S = A.s;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 
     uint64_t c_lo = A.c_lo, c_hi = A.c_hi, seg_chunks = A.seg_chunks, seg_end = A.seg_end;
     if (A.dev_tot) {
@@ -67,79 +83,89 @@ k_relax(RelaxArgs A) {
         seg_chunks = A.dev_tot[1];
         c_hi = seg_chunks;
     }
-    if (c_hi <= c_lo) return;
-    const uint64_t ntiles_seg = (seg_chunks + kTile - 1) / kTile;
-    const uint64_t t_first = c_lo / kTile, t_last = (c_hi - 1) / kTile;
-
-    for (uint64_t t = t_first + blockIdx.x; t <= t_last; t += gridDim.x) {
-        const uint64_t tb = t * kTile;
-        const uint64_t cb = tb > c_lo ? tb : c_lo;
-        const uint64_t ce = (tb + kTile) < c_hi ? (tb + kTile) : c_hi;
-        const uint64_t k0 = A.tile[t];
-        const uint64_t k1 = (t + 1 < ntiles_seg) ? (uint64_t)A.tile[t + 1] : seg_end - 1;
-        const int ne = (int)(k1 - k0 + 1);
-        __syncthreads();   // previous tile finished with smem
-        for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-            const uint64_t k = k0 + e;
-            const uint32_t v = A.qv[k];
-            s_pre[e] = A.qpre[k];
-            s_beg[e] = S.off[v];
-            s_end[e] = S.off[(uint64_t)v + 1];
-            if (ALGO == ALGO_PR) s_src[e] = __float_as_uint(A.qaux[k]);
-            else s_src[e] = __ldcg(&S.val[v]);
-        }
+    const uint32_t n_hot = PR ? (uint32_t)min((uint64_t)kHotV, S.V) : 0u;
+    if constexpr (PR) {
+        for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x) s_hot[i] = 0.0f;
         __syncthreads();
-
-        uint4 data[kChunksPerThread];
-        int ent[kChunksPerThread];
-        uint64_t absc[kChunksPerThread];
-#pragma unroll
-        for (int r = 0; r < kChunksPerThread; ++r) {
-            const uint64_t c = tb + (uint64_t)r * kRelaxThreads + threadIdx.x;
-            ent[r] = -1;
-            if (c >= cb && c < ce) {
-                int lo = 0, hi = ne - 1;          // largest e with s_pre[e] <= c
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_pre[mid] <= c) lo = mid; else hi = mid - 1;
-                }
-                const uint64_t j = c - s_pre[lo];
-                const uint64_t ac = chunk_lo(s_beg[lo], D1) + j;
-                const uint4 *p = COMPACT ? (A.base + (c - c_lo)) : (A.base + ((int64_t)ac - A.shift));
-                data[r] = *p;
-                ent[r] = lo;
-                absc[r] = ac;
+    }
+    if (c_hi > c_lo) {
+        const uint64_t ntiles_seg = (seg_chunks + kTile - 1) / kTile;
+        const uint64_t t_first = c_lo / kTile, t_last = (c_hi - 1) / kTile;
+        const uint64_t gw = (uint64_t)blockIdx.x * kWarps + w, nw = (uint64_t)gridDim.x * kWarps;
+        for (uint64_t t = t_first + gw; t <= t_last; t += nw) {
+            const uint64_t tb = t * kTile;
+            const uint64_t cb = tb > c_lo ? tb : c_lo;
+            const uint64_t ce = (tb + kTile) < c_hi ? (tb + kTile) : c_hi;
+            const uint64_t k0 = A.tile[t];
+            const uint64_t k1 = (t + 1 < ntiles_seg) ? (uint64_t)A.tile[t + 1] : seg_end - 1;
+            const int ne = (int)(k1 - k0 + 1);
+            for (int e = lane; e < ne; e += 32) {
+                const uint64_t k = k0 + e;
+                s_pre[w][e] = A.qpre[k];
+                s_beg[w][e] = A.qbeg[k];
+                s_deg[w][e] = A.qdeg[k];
+                s_src[w][e] = PR ? __float_as_uint(A.qaux[k]) : __ldcg(&S.val[A.qv[k]]);
             }
-        }
+            __syncwarp();
+            uint4 data[kChunksPerThread];
+            int ent[kChunksPerThread];
+            uint64_t absc[kChunksPerThread];
 #pragma unroll
-        for (int r = 0; r < kChunksPerThread; ++r) {
-            if (ent[r] < 0) continue;
-            const int e = ent[r];
-            const uint64_t beg = s_beg[e], end = s_end[e];
-            const uint32_t src = s_src[e];
-            const uint32_t words[4] = {data[r].x, data[r].y, data[r].z, data[r].w};
+            for (int r = 0; r < kChunksPerThread; ++r) {
+                const uint64_t c = tb + (uint64_t)r * 32 + lane;
+                ent[r] = -1;
+                if (c >= cb && c < ce) {
+                    int lo = 0, hi = ne - 1;          // largest e with s_pre[e] <= c
+                    while (lo < hi) {
+                        const int mid = (lo + hi + 1) >> 1;
+                        if (s_pre[w][mid] <= c) lo = mid; else hi = mid - 1;
+                    }
+                    const uint64_t ac = chunk_lo(s_beg[w][lo], D1) + (c - s_pre[w][lo]);
+                    const uint4 *p = COMPACT ? (A.base + (c - c_lo)) : (A.base + ((int64_t)ac - A.shift));
+                    data[r] = *p;
+                    ent[r] = lo;
+                    absc[r] = ac;
+                }
+            }
 #pragma unroll
-            for (int qd = 0; qd < EPC; ++qd) {
-                const uint64_t idx = absc[r] * EPC + qd;
-                if (idx < beg || idx >= end) continue;
-                uint32_t dst, wgt = 0;
-                if (D1 == 8) { dst = words[2 * qd]; wgt = words[2 * qd + 1]; }
-                else dst = words[qd];
-                if (ALGO == ALGO_PR) {
-                    atomicAdd(&S.delta[dst], __uint_as_float(src));
-                } else {
-                    uint32_t cand;
-                    if (ALGO == ALGO_BFS) cand = src + 1u;
-                    else if (ALGO == ALGO_SSSP) {
-                        const uint64_t c64 = (uint64_t)src + wgt;
-                        cand = c64 >= kInf ? kInf - 1u : (uint32_t)c64;
-                    } else cand = src;
-                    if (cand < __ldcg(&S.val[dst])) {
-                        const uint32_t old = atomicMin(&S.val[dst], cand);
-                        if (cand < old) atomicOr(&S.bm_next[dst >> 5], 1u << (dst & 31));
+            for (int r = 0; r < kChunksPerThread; ++r) {
+                if (ent[r] < 0) continue;
+                const int e = ent[r];
+                const uint64_t beg = s_beg[w][e], end = beg + s_deg[w][e];
+                const uint32_t src = s_src[w][e];
+                const uint32_t words[4] = {data[r].x, data[r].y, data[r].z, data[r].w};
+#pragma unroll
+                for (int qd = 0; qd < EPC; ++qd) {
+                    const uint64_t idx = absc[r] * EPC + qd;
+                    if (idx < beg || idx >= end) continue;
+                    uint32_t dst, wgt = 0;
+                    if (D1 == 8) { dst = words[2 * qd]; wgt = words[2 * qd + 1]; }
+                    else dst = words[qd];
+                    if constexpr (PR) {
+                        if (dst < n_hot) atomicAdd(&s_hot[dst], __uint_as_float(src));
+                        else atomicAdd(&S.delta[dst], __uint_as_float(src));
+                    } else {
+                        uint32_t cand;
+                        if (ALGO == ALGO_BFS) cand = src + 1u;
+                        else if (ALGO == ALGO_SSSP) {
+                            const uint64_t c64 = (uint64_t)src + wgt;
+                            cand = c64 >= kInf ? kInf - 1u : (uint32_t)c64;
+                        } else cand = src;
+                        if (cand < __ldcg(&S.val[dst])) {
+                            const uint32_t old = atomicMin(&S.val[dst], cand);
+                            if (cand < old) atomicOr(&S.bm_next[dst >> 5], 1u << (dst & 31));
+                        }
                     }
                 }
             }
+            __syncwarp();
+        }
+    }
+    if constexpr (PR) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x) {
+            const float x = s_hot[i];
+            if (x != 0.0f) atomicAdd(&S.delta[i], x);
         }
     }
 }
@@ -148,14 +174,16 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
                   const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st) {
     RelaxArgs A;
-    A.s = s; A.qv = q.qv; A.qpre = q.qpre; A.qaux = q.qaux; A.tile = q.tile + tile_base;
+    A.s = s; A.qv = q.qv; A.qpre = q.qpre; A.qbeg = q.qbeg; A.qdeg = q.qdeg; A.qaux = q.qaux;
+    A.tile = q.tile + tile_base;
     A.c_lo = c_lo; A.c_hi = c_hi; A.seg_chunks = seg_chunks; A.seg_first = seg_first; A.seg_end = seg_end;
     A.dev_tot = dev_tot; A.base = src.base; A.shift = src.shift;
     uint64_t grid;
     if (dev_tot) grid = (uint64_t)max_ctas;
     else {
         if (c_hi <= c_lo) return;
-        grid = (c_hi - 1) / kTile - c_lo / kTile + 1;
+        const uint64_t tiles = (c_hi - 1) / kTile - c_lo / kTile + 1;
+        grid = (tiles + kWarps - 1) / kWarps;
         if (grid > (uint64_t)max_ctas) grid = (uint64_t)max_ctas;
     }
     if (grid == 0) grid = 1;

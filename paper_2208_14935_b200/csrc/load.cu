@@ -6,10 +6,59 @@
 #include <cub/cub.cuh>
 #include <algorithm>
 #include <cstring>
+#include <mutex>
+#include <sys/mman.h>
 #include <thread>
+#include <unordered_map>
 #include "graph.h"
 
 namespace hyt {
+
+// ---------------------------------------------------------------------------
+// pinned mapped host memory
+// ---------------------------------------------------------------------------
+static std::mutex g_pin_mu;
+static std::unordered_map<void *, uint64_t> g_pinned;
+
+void *pinned_alloc(uint64_t bytes) {
+    const uint64_t huge = 2ull << 20;
+    const uint64_t len = (bytes + huge - 1) / huge * huge;
+    void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) throw Err{HYT_ENOMEM, "mmap of " + std::to_string(len) + " B failed"};
+    madvise(p, len, MADV_HUGEPAGE);
+    // parallel first touch (the registration pins resident pages)
+    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (len < (256ull << 20)) nt = 1;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        const uint64_t a = len / huge * t / nt * huge, b = len / huge * (t + 1) / nt * huge;
+        th.emplace_back([=] { std::memset((char *)p + a, 0, b - a); });
+    }
+    for (auto &x : th) x.join();
+    cudaError_t e = cudaHostRegister(p, len, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, len);
+        throw Err{HYT_ENOMEM, std::string("cudaHostRegister failed: ") + cudaGetErrorString(e)};
+    }
+    std::lock_guard<std::mutex> l(g_pin_mu);
+    g_pinned[p] = len;
+    return p;
+}
+
+void pinned_free(void *p) {
+    if (!p) return;
+    uint64_t len = 0;
+    {
+        std::lock_guard<std::mutex> l(g_pin_mu);
+        auto it = g_pinned.find(p);
+        if (it == g_pinned.end()) return;
+        len = it->second;
+        g_pinned.erase(it);
+    }
+    cudaHostUnregister(p);
+    munmap(p, len);
+}
 
 // ---------------------------------------------------------------------------
 // kernels
@@ -249,12 +298,10 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
 
         // ---- pinned mapped edge store (16-B padded so chunk loads never overrun) ----
         const uint64_t nbytes = ((E * 4 + 15) & ~15ull) + 32;
-        HYT_CUDA(cudaHostAlloc((void **)&g->nbr_h, nbytes, cudaHostAllocMapped | cudaHostAllocPortable));
-        std::memset((char *)g->nbr_h + E * 4, 0, nbytes - E * 4);
+        g->nbr_h = (uint32_t *)pinned_alloc(nbytes);      // zero-filled (padding included)
         if (w) {
             const uint64_t wbytes = ((E * 8 + 15) & ~15ull) + 32;
-            HYT_CUDA(cudaHostAlloc((void **)&g->ew_h, wbytes, cudaHostAllocMapped | cudaHostAllocPortable));
-            std::memset((char *)g->ew_h + E * 8, 0, wbytes - E * 8);
+            g->ew_h = (uint64_t *)pinned_alloc(wbytes);
         }
         uint32_t *nbr_out = nullptr;
         uint64_t *ew_out = nullptr;

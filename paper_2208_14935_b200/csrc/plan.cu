@@ -256,6 +256,8 @@ __device__ __forceinline__ void warp_write(const DevState &s, uint64_t ws, uint3
             const uint64_t pre = run_c + inc - nch;
             q.qv[idx] = (uint32_t)v;
             q.qpre[idx] = pre;
+            q.qbeg[idx] = o0;
+            q.qdeg[idx] = (uint32_t)deg;
             if (PR && !TAKE_DELTA) q.qaux[idx] = s.damping * scratch[v - v_lo] / (float)deg;
             write_tiles(q.tile + tile_base, pre, nch, (uint32_t)idx);
         }
@@ -394,14 +396,14 @@ __global__ void __launch_bounds__(kItemThreads) k_range_fill(DevState s, uint64_
 }
 
 // PR: take the delta of queue entries [e_lo, e_hi) right before their task runs.
-__global__ void k_take_delta(DevState s, const uint32_t *__restrict__ qv, float *__restrict__ qaux, uint64_t e_lo,
-                             uint64_t e_hi) {
+__global__ void k_take_delta(DevState s, const uint32_t *__restrict__ qv, const uint32_t *__restrict__ qdeg,
+                             float *__restrict__ qaux, uint64_t e_lo, uint64_t e_hi) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t k = e_lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < e_hi; k += stride) {
         const uint32_t v = qv[k];
         const float dl = atomicExch(&s.delta[v], 0.0f);
         s.rank[v] += dl;
-        qaux[k] = s.damping * dl / (float)(s.off[(uint64_t)v + 1] - s.off[v]);
+        qaux[k] = s.damping * dl / (float)qdeg[k];
     }
 }
 
@@ -409,7 +411,7 @@ void launch_take_delta(const DevState &s, const QueueBufs &q, uint64_t e_lo, uin
     if (e_hi <= e_lo) return;
     uint64_t blocks = (e_hi - e_lo + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
-    k_take_delta<<<(unsigned)blocks, 256, 0, st>>>(s, q.qv, q.qaux, e_lo, e_hi);
+    k_take_delta<<<(unsigned)blocks, 256, 0, st>>>(s, q.qv, q.qdeg, q.qaux, e_lo, e_hi);
 }
 
 void launch_range_queue(const DevState &s, uint64_t v_lo, uint64_t v_hi, RangeBufs r, cudaStream_t st) {
