@@ -426,7 +426,7 @@ def main():
         "roofline": roof,
         "kernels": kernels,
         "host_link": host_link,
-        "engine_ms": {tags[i]: float(eng_ms[i]) for i in range(7)},
+        "engine_ms": {tags[i]: float(eng_ms[i]) for i in range(8)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),

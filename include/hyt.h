@@ -93,7 +93,8 @@ typedef struct {
     uint64_t kernel_launches;      /* CUDA kernels this library launched in the run */
     /* Per activity tag: 0 plan (activity/selection/fill), 1 filter relax,
      * 2 compaction relax, 3 zero-copy relax, 4 resident relax, 5 filter
-     * recompute pass, 6 host-to-device copies.  Times are sums of per-launch
+     * recompute pass (relax), 6 host-to-device copies, 7 recompute queue
+     * building (k_range_count/fill).  Times are sums of per-launch
      * CUDA-event durations on the launching stream. */
     double   eng_ms[8];
     uint64_t eng_launches[8];

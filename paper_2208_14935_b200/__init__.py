@@ -33,7 +33,7 @@ ALGOS = {"bfs": HYT_BFS, "sssp": HYT_SSSP, "cc": HYT_CC, "pr": HYT_PR}
 HYT_NO_HUBSORT = 1
 MODES = {"hybrid": 0, "filter": 1, "compaction": 2, "zerocopy": 3, "resident": 4}
 HYT_ENG_NONE, HYT_ENG_F, HYT_ENG_C, HYT_ENG_Z, HYT_ENG_R = 0, 1, 2, 3, 4
-TAGS = ["plan", "filter", "compaction", "zerocopy", "resident", "recompute", "copy", "unused"]
+TAGS = ["plan", "filter", "compaction", "zerocopy", "resident", "recompute", "copy", "recompute_queue"]
 INF32 = 0xFFFFFFFF
 
 

@@ -200,7 +200,7 @@ class Pool {
 // run context (cached per handle and edge-record width)
 // ---------------------------------------------------------------------------
 struct EvPair { cudaEvent_t a, b; int tag; };
-enum Tag { TAG_PLAN = 0, TAG_F = 1, TAG_C = 2, TAG_Z = 3, TAG_R = 4, TAG_RECOMP = 5, TAG_COPY = 6 };
+enum Tag { TAG_PLAN = 0, TAG_F = 1, TAG_C = 2, TAG_Z = 3, TAG_R = 4, TAG_RECOMP = 5, TAG_COPY = 6, TAG_RQ = 7 };
 
 struct RunCtx {
     uint32_t d1 = 0;
@@ -232,6 +232,7 @@ struct RunCtx {
     uint32_t *snap = nullptr;     // multi-GPU: own-range values before the exchange
     uint64_t *red = nullptr;      // multi-GPU: device scratch for the active-count reduction
     uint64_t *racc = nullptr;     // recompute statistics accumulators (u64[4])
+    uint32_t *outbuf = nullptr;   // u32[V] result staging for hyt_get_values
     uint64_t v_lo = 0, v_hi = 0;  // own vertex range
     std::vector<void *> dev;      // arena blocks (released with the context)
     std::vector<void *> pinned;   // cudaHostAlloc blocks
@@ -285,6 +286,7 @@ static void harvest(hyt_graph *g, RunCtx *c) {
             case TAG_PLAN: t = &g->plan_time; break;
             case TAG_RECOMP: t = &g->recompute_time; break;
             case TAG_COPY: t = &g->copy_time; break;
+            case TAG_RQ: t = &g->rq_time; break;
             default: t = &g->eng_time[ep.tag]; break;
         }
         t->ms += ms;
@@ -320,6 +322,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->v_hi = c->bounds[c->p_hi];
         c->red = dalloc<uint64_t>(g, c, 2, "reduction scratch");
         c->racc = dalloc<uint64_t>(g, c, 4, "recompute statistics");
+        c->outbuf = dalloc<uint32_t>(g, c, V, "result staging");
         if (g->world > 1 && algo != ALGO_PR)
             c->snap = dalloc<uint32_t>(g, c, c->v_hi - c->v_lo + 1, "exchange snapshot");
         // ---- vertex state (the paper assumes it fits) ----
@@ -576,7 +579,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     g->stats = hyt_stats{};
     g->iter_log.clear();
     for (auto &t : g->eng_time) t = EngTime{};
-    g->recompute_time = g->copy_time = g->plan_time = EngTime{};
+    g->recompute_time = g->copy_time = g->plan_time = g->rq_time = EngTime{};
     for (int i = 0; i < ENG_COUNT; ++i) g->eng_chunks[i] = g->eng_edges[i] = 0;
     g->has_result = false;
 
@@ -593,6 +596,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         if (c->v_lo) HYT_CUDA(cudaMemsetAsync(c->delta, 0, c->v_lo * 4, main));
         if (c->v_hi < g->V) HYT_CUDA(cudaMemsetAsync(c->delta + c->v_hi, 0, (g->V - c->v_hi) * 4, main));
     }
+    HYT_CUDA(cudaMemsetAsync(c->racc, 0, 4 * sizeof(uint64_t), main));
     g->launches = 1;
 
     const uint64_t np = c->p_hi - c->p_lo;
@@ -690,8 +694,11 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                          nullptr, es, relax_ctas, stm);
             timed_end(c, stm, e2);
             if (P.recompute) {   // process the loaded unit exactly once more
-                timed_begin(c, stm, e3, TAG_RECOMP);
+                EvPair e4;
+                timed_begin(c, stm, e4, TAG_RQ);
                 launch_range_queue(s, v_lo, v_hi, c->rb[si], stm);
+                timed_end(c, stm, e4);
+                timed_begin(c, stm, e3, TAG_RECOMP);
                 launch_relax(s, c->rb[si].q, 0, 0, 0, 0, 0, 0, c->rb[si].total, es, relax_ctas, stm);
                 timed_end(c, stm, e3);
             }
@@ -839,6 +846,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         g->stats.eng_edges[5] = racc[2];
     }
     g->stats.eng_ms[6] = g->copy_time.ms; g->stats.eng_launches[6] = g->copy_time.launches;
+    g->stats.eng_ms[7] = g->rq_time.ms; g->stats.eng_launches[7] = g->rq_time.launches;
     g->val_d = c->val; g->rank_d = c->rank; g->delta_d = c->delta;
     g->last_algo = algo;
     g->has_result = true;
@@ -854,13 +862,9 @@ void get_values(hyt_graph *g, void *out, uint64_t count) {
     RunCtx *c = ctx_of(g, g->last_algo);
     HYT_REQUIRE(c != nullptr, HYT_ESTATE, "no result: run context was released");
     DevState s = make_state(g, c);
-    uint32_t *tmp = arena_new<uint32_t>(g->arena, g->V, "result staging");
-    launch_gather_out(s, g->new_id_d, tmp, g->main);
-    cudaError_t e1 = cudaMemcpyAsync(out, tmp, g->V * 4, cudaMemcpyDeviceToHost, g->main);
-    cudaError_t e2 = cudaStreamSynchronize(g->main);
-    g->arena.release(tmp);
-    HYT_CUDA(e1);
-    HYT_CUDA(e2);
+    launch_gather_out(s, g->new_id_d, c->outbuf, g->main);
+    HYT_CUDA(cudaMemcpyAsync(out, c->outbuf, g->V * 4, cudaMemcpyDeviceToHost, g->main));
+    HYT_CUDA(cudaStreamSynchronize(g->main));
 }
 
 // ---------------------------------------------------------------------------

@@ -115,7 +115,7 @@ struct hyt_graph {
     hyt_stats stats{};
     std::vector<hyt_iter> iter_log;
     hyt::EngTime eng_time[hyt::ENG_COUNT];
-    hyt::EngTime recompute_time, copy_time, plan_time;
+    hyt::EngTime recompute_time, copy_time, plan_time, rq_time;
     uint64_t eng_chunks[hyt::ENG_COUNT] = {0, 0, 0, 0, 0};
     uint64_t eng_edges[hyt::ENG_COUNT] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
