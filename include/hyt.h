@@ -153,7 +153,12 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   delta for PR, hub otherwise; 0 none, 1 hub, 2 delta];
  *   recompute [1] (process a loaded filter unit once more);
  *   damping [0.85], epsilon [1e-6], max_iters [1000] (PR);
- *   gather_threads [0 = all cores]; compaction_buffer_bytes [0 = auto].
+ *   gather_threads [0 = all cores]; compaction_buffer_bytes [0 = auto];
+ *   edge_cache [0]: 1 keeps the longest hub-order prefix of partitions that fits
+ *   the budget left after the run buffers resident in device memory (served as
+ *   engine R at no transfer cost, beyond the paper, whose edges
+ *   are re-transferred every iteration); edge_cache_bytes [0 = no cap]
+ *   caps its size.
  * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
 int hyt_set_param(hyt_graph *g, const char *key, double value);
 

@@ -233,6 +233,8 @@ struct RunCtx {
     uint64_t *red = nullptr;      // multi-GPU: device scratch for the active-count reduction
     uint64_t *racc = nullptr;     // recompute statistics accumulators (u64[4])
     uint32_t *outbuf = nullptr;   // u32[V] result staging for hyt_get_values
+    uint4 *cache = nullptr;       // resident edge cache: chunks [cache_c0, ...) of partitions [p_lo, cache_hi)
+    uint64_t cache_c0 = 0, cache_hi = 0, cache_bytes = 0;
     uint64_t v_lo = 0, v_hi = 0;  // own vertex range
     std::vector<void *> dev;      // arena blocks (released with the context)
     std::vector<void *> pinned;   // cudaHostAlloc blocks
@@ -305,6 +307,19 @@ template <class T> static T *halloc(RunCtx *c, uint64_t n) {
     void *p = pinned_alloc(n * sizeof(T) + 64);
     c->pinned.push_back(p);
     return (T *)p;
+}
+
+// Copy the edges of own partitions [p_lo, p_hi_cache) into device memory once;
+// the plan then serves them as the resident engine (cost 0, no transfer).
+static void fill_cache(hyt_graph *g, RunCtx *c, uint64_t p_hi_cache) {
+    const uint64_t c0 = chunk_lo(g->off_h[c->bounds[c->p_lo]], c->d1);
+    const uint64_t c1 = chunk_hi(g->off_h[c->bounds[p_hi_cache]], c->d1);
+    c->cache = dalloc<uint4>(g, c, c1 - c0 + 1, "resident edge cache");
+    const uint4 *src = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
+    HYT_CUDA(cudaMemcpy(c->cache, src + c0, (c1 - c0) * 16, cudaMemcpyHostToDevice));
+    c->cache_c0 = c0;
+    c->cache_hi = p_hi_cache;
+    c->cache_bytes = (c1 - c0) * 16;
 }
 
 static RunCtx *build_ctx(hyt_graph *g, int algo) {
@@ -401,18 +416,14 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         };
         spans(k);
         if (P.engine_mode == MODE_RESIDENT) {
-            // edges once into device memory, cached on the handle
-            const int which = c->d1 == 8 ? 1 : 0;
-            if (!g->res_edges[which]) {
-                const uint64_t bytes = chunk_hi(g->E, c->d1) * 16;   // within the 16-B padded store
-                g->res_edges[which] = arena_new<uint4>(g->arena, bytes / 16 + 2, "resident edges");
-                const void *src = which ? (const void *)g->ew_h : (const void *)g->nbr_h;
-                HYT_CUDA(cudaMemcpy(g->res_edges[which], src, bytes, cudaMemcpyHostToDevice));
-            }
+            // every own partition's edges once into device memory
+            fill_cache(g, c, c->p_hi);
         } else {
             const uint64_t rq_bytes_per_v = 28 + 4 + (algo == ALGO_PR ? 8 : 0);
             (void)rq_bytes_per_v;
-            auto range_bytes = [&]() { return max_part_v * rq_bytes_per_v + max_span / 16 / kTile * 4 + 65536; };
+            auto range_bytes = [&]() {
+                return max_part_v * rq_bytes_per_v + (max_span / 16 + max_part_v) / kTile * 4 + 65536;
+            };
             const uint64_t cmin = 4ull << 20;
             int S = std::max(1, std::min(P.streams, 8));
             // a small budget first drops streams, then merges fewer partitions per unit
@@ -431,7 +442,9 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 r.vcap = max_part_v + 64;
                 r.cta_cap = r.vcap / (32 * kItemWords) + 4;
                 r.q.cap = r.vcap;
-                r.q.tile_cap = max_span / 16 / kTile + 8;
+                // a range queue's chunk space can exceed the span: adjacent short lists
+                // that share a 16-B chunk each count it (<= one extra chunk per vertex)
+                r.q.tile_cap = (max_span / 16 + max_part_v) / kTile + 8;
                 r.q.qv = dalloc<uint32_t>(g, c, r.q.cap, "recompute queue");
                 r.q.qpre = dalloc<uint64_t>(g, c, r.q.cap, "recompute prefix");
                 r.q.qbeg = dalloc<uint64_t>(g, c, r.q.cap, "recompute edge begin");
@@ -449,7 +462,9 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
             uint64_t cb = P.compaction_buffer_bytes;
             if (!cb) {
                 const uint64_t av = g->arena.avail();
-                const uint64_t left = av == UINT64_MAX ? (1ull << 30) : (av > 8192 ? av / 2 - 4096 : 0);
+                // with the edge cache on, most of the leftover budget goes to the cache
+                const uint64_t div = P.edge_cache ? 16 : 2;
+                const uint64_t left = av == UINT64_MAX ? (1ull << 30) : (av > 8192 ? av / div - 4096 : 0);
                 cb = std::min<uint64_t>(256ull << 20, left);
             }
             cb = std::max<uint64_t>(cmin, cb) & ~15ull;
@@ -465,6 +480,18 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
             unsigned nt = P.gather_threads > 0 ? (unsigned)P.gather_threads
                                                : std::max(1u, std::thread::hardware_concurrency());
             c->pool = new Pool(nt);
+            if (P.edge_cache && P.engine_mode == MODE_HYBRID) {
+                // partial resident edge cache: the longest prefix of the
+                // own partitions in hub order that fits what the budget has left
+                const uint64_t av = g->arena.avail();
+                const uint64_t reserve = av == UINT64_MAX ? 0 : std::min<uint64_t>(64ull << 20, av / 16);
+                uint64_t room = av == UINT64_MAX ? UINT64_MAX : av - reserve;
+                if (P.edge_cache_bytes) room = std::min(room, P.edge_cache_bytes);
+                const uint64_t c0 = chunk_lo(g->off_h[c->bounds[c->p_lo]], c->d1);
+                uint64_t j = c->p_lo;
+                while (j < c->p_hi && (chunk_hi(g->off_h[c->bounds[j + 1]], c->d1) - c0) * 16 <= room) ++j;
+                if (j > c->p_lo) fill_cache(g, c, j);
+            }
         }
         // streams
         const int nst = std::max(c->S, 1) + 2;
@@ -573,7 +600,6 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     const uint4 *edges_host = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
     const uint4 *edges_mapped = nullptr;
     HYT_CUDA(cudaHostGetDevicePointer((void **)&edges_mapped, (void *)edges_host, 0));
-    const uint4 *edges_dev = g->res_edges[c->d1 == 8 ? 1 : 0];
 
     // reset statistics
     g->stats = hyt_stats{};
@@ -612,7 +638,8 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         HYT_CUDA(cudaMemsetAsync(c->hdr_d, 0, sizeof(SegHdr), main));
         HYT_CUDA(cudaMemsetAsync(c->parts_d + c->p_lo, 0, np * sizeof(PartIter), main));
         const PlanBufs pb{c->parts_d, c->iagg, c->ibase, c->hdr_d};
-        launch_plan(s, c->bounds_d, c->t_d, c->items, c->item_lo, c->item_hi, c->p_lo, c->p_hi, mode, cp, pb, main);
+        launch_plan(s, c->bounds_d, c->t_d, c->items, c->item_lo, c->item_hi, c->p_lo, c->p_hi, c->cache_hi, mode, cp,
+                    pb, main);
         launch_fill(s, c->bounds_d, c->items, c->item_lo, c->item_hi, pb, c->q, main);
         timed_end(c, main, ep);
         g->launches += (algo == ALGO_PR) ? 3 : 2;
@@ -725,11 +752,11 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         }
         // ---- resident (build extension) ----
         if (H.ent_count[ENG_R]) {
-            HYT_REQUIRE(edges_dev != nullptr, HYT_ESTATE, "resident edges missing");
+            HYT_REQUIRE(c->cache != nullptr, HYT_ESTATE, "resident edges missing");
             cudaStream_t stm = g->st[0];
             EvPair e1;
             timed_begin(c, stm, e1, TAG_R);
-            EdgeSrc es{edges_dev, 0, false};
+            EdgeSrc es{c->cache, (int64_t)c->cache_c0, false};
             if (algo == ALGO_PR) {
                 launch_take_delta(s, c->q, H.ent_base[ENG_R], H.ent_base[ENG_R] + H.ent_count[ENG_R], stm);
                 g->launches += 1;
@@ -902,8 +929,8 @@ void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_par
     HYT_CUDA(cudaMemsetAsync(c->hdr_d, 0, sizeof(SegHdr), g->main));
     HYT_CUDA(cudaMemsetAsync(c->parts_d, 0, N * sizeof(PartIter), g->main));
     const PlanBufs pb{c->parts_d, c->iagg, c->ibase, c->hdr_d};
-    launch_plan(s, c->bounds_d, c->t_d, c->items, 0, c->n_items, 0, N, g->prm.engine_mode, make_cost(g->prm, d1), pb,
-                g->main);
+    launch_plan(s, c->bounds_d, c->t_d, c->items, 0, c->n_items, 0, N, c->cache_hi, g->prm.engine_mode,
+                make_cost(g->prm, d1), pb, g->main);
     std::vector<PartIter> ph(N);
     HYT_CUDA(cudaMemcpyAsync(ph.data(), c->parts_d, N * sizeof(PartIter), cudaMemcpyDeviceToHost, g->main));
     HYT_CUDA(cudaStreamSynchronize(g->main));

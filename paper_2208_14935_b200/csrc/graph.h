@@ -68,6 +68,8 @@ struct Params {
     uint64_t compaction_buffer_bytes = 0;
     int zc_ctas_per_sm = 2;
     int relax_ctas_per_sm = 4;
+    int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
+    uint64_t edge_cache_bytes = 0;   // cap on the cache (0 = whatever the budget leaves)
 };
 
 CostParams make_cost(const Params &p, uint32_t d1);
@@ -101,8 +103,6 @@ struct hyt_graph {
     uint32_t *new_id_d = nullptr;   // caller id -> internal id
     uint32_t *old_of_d = nullptr;   // internal id -> caller id
     uint32_t *din_d = nullptr;      // in-degree (internal ids)
-    // resident edge cache (engine_mode = resident)
-    uint4 *res_edges[2] = {nullptr, nullptr};   // [0] ids, [1] packed (id,w)
     // ---- streams ----
     cudaStream_t main = nullptr;
     std::vector<cudaStream_t> st;   // worker streams

@@ -130,9 +130,10 @@ struct PlanBufs {
 
 // ---- kernel launchers (plan.cu, kernels.cu) ----
 void launch_pr_frontier(const DevState &s, cudaStream_t st);
+// Partitions [p_lo, cache_hi) have their edges resident in device memory (engine R).
 void launch_plan(const DevState &s, const uint64_t *bounds, const uint64_t *t_static, Items it,
-                 uint64_t item_lo, uint64_t item_hi, uint64_t p_lo, uint64_t p_hi, int mode, const CostParams &cp,
-                 PlanBufs pb, cudaStream_t st);
+                 uint64_t item_lo, uint64_t item_hi, uint64_t p_lo, uint64_t p_hi, uint64_t cache_hi, int mode,
+                 const CostParams &cp, PlanBufs pb, cudaStream_t st);
 void launch_fill(const DevState &s, const uint64_t *bounds, Items it, uint64_t item_lo, uint64_t item_hi,
                  PlanBufs pb, QueueBufs q, cudaStream_t st);
 // Edge source for a relax launch.

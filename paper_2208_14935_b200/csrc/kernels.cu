@@ -40,7 +40,8 @@ void launch_pr_frontier(const DevState &s, cudaStream_t st) {
 // space (warps are independent: no CTA barriers on the hot loop).  Per tile the
 // lanes stage the <= kTile+1 overlapping queue entries (prefix, first edge,
 // degree, source value) in the warp's shared-memory slice, then each lane finds
-// the entry of each of its 4 chunks by binary search and issues 4 independent
+// the entry of each of its 4 chunks from a 128-bit map of entry start positions
+// (one popc) and issues 4 independent
 // 16-byte loads; 8 consecutive lanes cover one aligned 128-byte line.
 // PR: pushes into the hub block (ids < kHotV, the highest-H vertices after hub
 // sorting) are accumulated in shared memory and flushed once per CTA, so
@@ -64,7 +65,7 @@ struct RelaxArgs {
 constexpr int kWarps = kRelaxThreads / 32;
 
 template <int ALGO, bool COMPACT>
-__global__ void __launch_bounds__(kRelaxThreads)
+__global__ void __launch_bounds__(kRelaxThreads, 4)
 k_relax(RelaxArgs A) {
     constexpr uint32_t D1 = (ALGO == ALGO_SSSP) ? 8u : 4u;
     constexpr int EPC = 16 / D1;                  // edge records per chunk
@@ -73,6 +74,7 @@ k_relax(RelaxArgs A) {
     __shared__ uint64_t s_beg[kWarps][kTile + 1];
     __shared__ uint32_t s_deg[kWarps][kTile + 1];
     __shared__ uint32_t s_src[kWarps][kTile + 1];
+    __shared__ uint32_t s_mask[kWarps][kChunksPerThread];
     __shared__ float s_hot[PR ? kHotV : 1];
     const DevState &S = A.s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -99,63 +101,110 @@ k_relax(RelaxArgs A) {
             const uint64_t k0 = A.tile[t];
             const uint64_t k1 = (t + 1 < ntiles_seg) ? (uint64_t)A.tile[t + 1] : seg_end - 1;
             const int ne = (int)(k1 - k0 + 1);
+            if (lane < kChunksPerThread) s_mask[w][lane] = 0u;
+            __syncwarp();
             for (int e = lane; e < ne; e += 32) {
                 const uint64_t k = k0 + e;
-                s_pre[w][e] = A.qpre[k];
+                const uint64_t pre = A.qpre[k];
+                s_pre[w][e] = pre;
                 s_beg[w][e] = A.qbeg[k];
                 s_deg[w][e] = A.qdeg[k];
                 s_src[w][e] = PR ? __float_as_uint(A.qaux[k]) : __ldcg(&S.val[A.qv[k]]);
+                // 128-bit map of the tile positions where an entry starts (the entry
+                // covering the tile's first chunk starts at position 0)
+                const uint64_t pos = pre > tb ? pre - tb : 0;
+                if (pos < (uint64_t)kTile) atomicOr(&s_mask[w][pos >> 5], 1u << (pos & 31));
             }
             __syncwarp();
             uint4 data[kChunksPerThread];
             int ent[kChunksPerThread];
             uint64_t absc[kChunksPerThread];
+            // lane L's r-th chunk is tile position 32 r + L: its entry index is the
+            // number of starts at positions <= 32 r + L, minus one
+            const uint32_t le = 0xFFFFFFFFu >> (31 - lane);
+            int before = 0;
 #pragma unroll
             for (int r = 0; r < kChunksPerThread; ++r) {
+                const uint32_t m = s_mask[w][r];
                 const uint64_t c = tb + (uint64_t)r * 32 + lane;
+                const int e = before + __popc(m & le) - 1;
+                before += __popc(m);
                 ent[r] = -1;
                 if (c >= cb && c < ce) {
-                    int lo = 0, hi = ne - 1;          // largest e with s_pre[e] <= c
-                    while (lo < hi) {
-                        const int mid = (lo + hi + 1) >> 1;
-                        if (s_pre[w][mid] <= c) lo = mid; else hi = mid - 1;
-                    }
-                    const uint64_t ac = chunk_lo(s_beg[w][lo], D1) + (c - s_pre[w][lo]);
+                    const uint64_t ac = chunk_lo(s_beg[w][e], D1) + (c - s_pre[w][e]);
                     const uint4 *p = COMPACT ? (A.base + (c - c_lo)) : (A.base + ((int64_t)ac - A.shift));
                     data[r] = *p;
-                    ent[r] = lo;
+                    ent[r] = e;
                     absc[r] = ac;
                 }
             }
+            if constexpr (PR) {
 #pragma unroll
-            for (int r = 0; r < kChunksPerThread; ++r) {
-                if (ent[r] < 0) continue;
-                const int e = ent[r];
-                const uint64_t beg = s_beg[w][e], end = beg + s_deg[w][e];
-                const uint32_t src = s_src[w][e];
-                const uint32_t words[4] = {data[r].x, data[r].y, data[r].z, data[r].w};
+                for (int r = 0; r < kChunksPerThread; ++r) {
+                    if (ent[r] < 0) continue;
+                    const int e = ent[r];
+                    const uint64_t base = absc[r] * EPC, beg = s_beg[w][e];
+                    // valid edge slots of this chunk: [lo, hi) (32-bit after one 64-bit step)
+                    const int lo = beg > base ? (int)(beg - base) : 0;
+                    const uint64_t end = beg + s_deg[w][e];
+                    const int hi = end - base < (uint64_t)EPC ? (int)(end - base) : EPC;
+                    const float x = __uint_as_float(s_src[w][e]);
+                    const uint32_t words[4] = {data[r].x, data[r].y, data[r].z, data[r].w};
 #pragma unroll
-                for (int qd = 0; qd < EPC; ++qd) {
-                    const uint64_t idx = absc[r] * EPC + qd;
-                    if (idx < beg || idx >= end) continue;
-                    uint32_t dst, wgt = 0;
-                    if (D1 == 8) { dst = words[2 * qd]; wgt = words[2 * qd + 1]; }
-                    else dst = words[qd];
-                    if constexpr (PR) {
-                        if (dst < n_hot) atomicAdd(&s_hot[dst], __uint_as_float(src));
-                        else atomicAdd(&S.delta[dst], __uint_as_float(src));
-                    } else {
-                        uint32_t cand;
-                        if (ALGO == ALGO_BFS) cand = src + 1u;
-                        else if (ALGO == ALGO_SSSP) {
-                            const uint64_t c64 = (uint64_t)src + wgt;
-                            cand = c64 >= kInf ? kInf - 1u : (uint32_t)c64;
-                        } else cand = src;
-                        if (cand < __ldcg(&S.val[dst])) {
-                            const uint32_t old = atomicMin(&S.val[dst], cand);
-                            if (cand < old) atomicOr(&S.bm_next[dst >> 5], 1u << (dst & 31));
+                    for (int qd = 0; qd < EPC; ++qd) {
+                        if (qd < lo || qd >= hi) continue;
+                        const uint32_t dst = words[qd];
+                        if (dst < n_hot) atomicAdd(&s_hot[dst], x);
+                        else atomicAdd(&S.delta[dst], x);
+                    }
+                }
+            } else {
+                // two halves of two chunks: gather every destination value first (up
+                // to 8 loads in flight per lane), then compare and update
+#pragma unroll
+                for (int h = 0; h < kChunksPerThread; h += 2) {
+                    uint32_t dst[2][EPC], cand[2][EPC], cur[2][EPC];
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr) {
+                        const int r = h + rr;
+                        int lo = EPC, hi = 0;
+                        uint32_t src = 0;
+                        if (ent[r] >= 0) {
+                            const int e = ent[r];
+                            const uint64_t base = absc[r] * EPC, beg = s_beg[w][e];
+                            lo = beg > base ? (int)(beg - base) : 0;
+                            const uint64_t end = beg + s_deg[w][e];
+                            hi = end - base < (uint64_t)EPC ? (int)(end - base) : EPC;
+                            src = s_src[w][e];
+                        }
+                        const uint32_t words[4] = {data[r].x, data[r].y, data[r].z, data[r].w};
+#pragma unroll
+                        for (int qd = 0; qd < EPC; ++qd) {
+                            const bool ok = qd >= lo && qd < hi;
+                            uint32_t d, wgt = 0;
+                            if (D1 == 8) { d = words[2 * qd]; wgt = words[2 * qd + 1]; }
+                            else d = words[qd];
+                            uint32_t cnd;
+                            if (ALGO == ALGO_BFS) cnd = src + 1u;
+                            else if (ALGO == ALGO_SSSP) {
+                                const uint64_t c64 = (uint64_t)src + wgt;
+                                cnd = c64 >= kInf ? kInf - 1u : (uint32_t)c64;
+                            } else cnd = src;
+                            dst[rr][qd] = d;
+                            cand[rr][qd] = ok ? cnd : kInf;
+                            cur[rr][qd] = ok ? __ldcg(&S.val[d]) : 0u;
                         }
                     }
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+                        for (int qd = 0; qd < EPC; ++qd) {
+                            const uint32_t d = dst[rr][qd], cnd = cand[rr][qd];
+                            if (cnd < cur[rr][qd]) {
+                                const uint32_t old = atomicMin(&S.val[d], cnd);
+                                if (cnd < old) atomicOr(&S.bm_next[d >> 5], 1u << (d & 31));
+                            }
+                        }
                 }
             }
             __syncwarp();

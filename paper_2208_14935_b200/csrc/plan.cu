@@ -27,7 +27,7 @@ struct PlanArgs {
     DevState s;
     const uint64_t *bounds, *t_static;
     Items it;
-    uint64_t item_lo, item_hi, p_lo, p_hi;
+    uint64_t item_lo, item_hi, p_lo, p_hi, cache_hi;
     int mode;
     CostParams cp;
     PlanBufs pb;
@@ -112,7 +112,9 @@ __global__ void __launch_bounds__(kItemThreads) k_plan_items(PlanArgs A) {
         PartIter *P = &A.pb.parts[pi];
         const uint64_t pe = __ldcg(&P->e), pa = __ldcg(&P->a), pz = __ldcg(&P->z);
         int p = ENG_NONE;
-        if (pe > 0) {
+        if (pe > 0 && pi < A.cache_hi) {
+            p = ENG_R;                   // edges resident in device memory: no transfer
+        } else if (pe > 0) {
             switch (A.mode) {
                 case MODE_HYBRID: p = select_engine(A.t_static[pi], pe, pa, pz, A.cp); break;
                 case MODE_FILTER: p = ENG_F; break;
@@ -306,12 +308,12 @@ __global__ void __launch_bounds__(kItemThreads) k_fill_items(FillArgs A) {
 }
 
 void launch_plan(const DevState &s, const uint64_t *bounds, const uint64_t *t_static, Items it,
-                 uint64_t item_lo, uint64_t item_hi, uint64_t p_lo, uint64_t p_hi, int mode, const CostParams &cp,
-                 PlanBufs pb, cudaStream_t st) {
+                 uint64_t item_lo, uint64_t item_hi, uint64_t p_lo, uint64_t p_hi, uint64_t cache_hi, int mode,
+                 const CostParams &cp, PlanBufs pb, cudaStream_t st) {
     if (item_hi <= item_lo) return;
     PlanArgs A;
     A.s = s; A.bounds = bounds; A.t_static = t_static; A.it = it;
-    A.item_lo = item_lo; A.item_hi = item_hi; A.p_lo = p_lo; A.p_hi = p_hi;
+    A.item_lo = item_lo; A.item_hi = item_hi; A.p_lo = p_lo; A.p_hi = p_hi; A.cache_hi = cache_hi;
     A.mode = mode; A.cp = cp; A.pb = pb;
     const unsigned grid = (unsigned)(item_hi - item_lo);
     if (s.algo == ALGO_PR) k_plan_items<true><<<grid, kItemThreads, 0, st>>>(A);

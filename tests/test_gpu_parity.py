@@ -292,3 +292,42 @@ def test_errors(hyt):
         G2.close()
     finally:
         G.close()
+
+
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+def test_partial_edge_cache(hyt, algo):
+    """edge_cache=1: a hub-order prefix of partitions is served from
+    device memory (engine R), the rest by the hybrid engines; results unchanged."""
+    gkey = ("rmat", 9)
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    d1 = 8 if algo == "sssp" else 4
+    # cache about half of the edge bytes: the rest still goes through the hybrid engines
+    got, st, log = run_gpu(hyt, g, algo, part=4096, edge_cache=1, edge_cache_bytes=g.E * d1 // 2)
+    want = expected(gkey, algo)
+    if algo == "pr":
+        assert_pr_close(got, want)
+    else:
+        assert np.array_equal(got, want)
+    assert st["parts_resident"] > 0
+    assert st["parts_filter"] + st["parts_compaction"] + st["parts_zerocopy"] > 0
+
+
+@pytest.mark.parametrize("engine", ["filter", "hybrid", "compaction", "zerocopy"])
+def test_many_short_lists_large_units(hyt, engine):
+    """Regression: 200K vertices of out-degree 1-2 inside 1 MiB partitions.  A unit's
+    recompute queue then has more 16-B chunks than its span (adjacent short lists
+    share chunks), which once overflowed the recompute tile map."""
+    rng = np.random.default_rng(5)
+    V = 200_000
+    src = np.concatenate([np.arange(V), np.arange(0, V, 3)])
+    dst = rng.integers(0, V, size=len(src))
+    g = hytgen.csr_from_edges(V, src, dst, weighted=True, name="short_lists")
+    for algo in ("sssp", "bfs", "pr"):
+        got, _, _ = run_gpu(hyt, g, algo, engine=engine, part=1 << 20)
+        if algo == "pr":
+            want, _ = oracle.pr_jacobi(g.off, g.nbr, tol=1e-12)
+            assert_pr_close(got, want)
+        elif algo == "sssp":
+            assert np.array_equal(got, oracle.sssp(g.off, g.nbr, g.w, 0))
+        else:
+            assert np.array_equal(got, oracle.bfs(g.off, g.nbr, 0))
