@@ -64,6 +64,34 @@ struct RelaxArgs {
 
 constexpr int kWarps = kRelaxThreads / 32;
 
+// L2 eviction-priority hints: the edge stream is read once per task (evict first),
+// the vertex values / deltas are re-read by every task (evict last), so the
+// streaming edges do not push the value array out of the 126 MB L2.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint4 ld_stream(const uint4 *p, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_keep(const uint32_t *p, uint64_t pol) {
+    uint32_t r;
+    asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void red_add_keep(float *p, float x, uint64_t pol) {
+    asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(x), "l"(pol) : "memory");
+}
+
 template <int ALGO, bool COMPACT>
 __global__ void __launch_bounds__(kRelaxThreads, 4)
 k_relax(RelaxArgs A) {
@@ -78,6 +106,7 @@ k_relax(RelaxArgs A) {
     __shared__ float s_hot[PR ? kHotV : 1];
     const DevState &S = A.s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
 
     uint64_t c_lo = A.c_lo, c_hi = A.c_hi, seg_chunks = A.seg_chunks, seg_end = A.seg_end;
     if (A.dev_tot) {
@@ -109,7 +138,7 @@ k_relax(RelaxArgs A) {
                 s_pre[w][e] = pre;
                 s_beg[w][e] = A.qbeg[k];
                 s_deg[w][e] = A.qdeg[k];
-                s_src[w][e] = PR ? __float_as_uint(A.qaux[k]) : __ldcg(&S.val[A.qv[k]]);
+                s_src[w][e] = PR ? __float_as_uint(A.qaux[k]) : ld_keep(&S.val[A.qv[k]], pol_keep);
                 // 128-bit map of the tile positions where an entry starts (the entry
                 // covering the tile's first chunk starts at position 0)
                 const uint64_t pos = pre > tb ? pre - tb : 0;
@@ -133,7 +162,7 @@ k_relax(RelaxArgs A) {
                 if (c >= cb && c < ce) {
                     const uint64_t ac = chunk_lo(s_beg[w][e], D1) + (c - s_pre[w][e]);
                     const uint4 *p = COMPACT ? (A.base + (c - c_lo)) : (A.base + ((int64_t)ac - A.shift));
-                    data[r] = *p;
+                    data[r] = ld_stream(p, pol_stream);
                     ent[r] = e;
                     absc[r] = ac;
                 }
@@ -155,7 +184,7 @@ k_relax(RelaxArgs A) {
                         if (qd < lo || qd >= hi) continue;
                         const uint32_t dst = words[qd];
                         if (dst < n_hot) atomicAdd(&s_hot[dst], x);
-                        else atomicAdd(&S.delta[dst], x);
+                        else red_add_keep(&S.delta[dst], x, pol_keep);
                     }
                 }
             } else {
@@ -192,7 +221,7 @@ k_relax(RelaxArgs A) {
                             } else cnd = src;
                             dst[rr][qd] = d;
                             cand[rr][qd] = ok ? cnd : kInf;
-                            cur[rr][qd] = ok ? __ldcg(&S.val[d]) : 0u;
+                            cur[rr][qd] = ok ? ld_keep(&S.val[d], pol_keep) : 0u;
                         }
                     }
 #pragma unroll

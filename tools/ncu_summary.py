@@ -41,7 +41,7 @@ def launches(path):
             continue
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "")
-        us = v / 1e3 if unit == "nsecond" else v * 1e3 if unit == "msecond" else v
+        us = v / 1e3 if unit in ("nsecond", "ns") else v * 1e3 if unit in ("msecond", "ms") else v
         rows.append((short(r["Kernel Name"]), us))
     tot = sum(u for _, u in rows)
     agg = defaultdict(lambda: [0, 0.0])
