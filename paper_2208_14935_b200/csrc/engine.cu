@@ -85,6 +85,9 @@ CostParams make_cost(const Params &p, uint32_t d1) {
     c.an = (uint64_t)(p.alpha * den + 0.5); c.ad = den;
     c.bn = (uint64_t)(p.beta * den + 0.5); c.bd = den;
     c.gn = (uint64_t)(p.gamma * den + 0.5); c.gd = den;
+    c.m_shift = -1;
+    for (int k = 0; k < 63; ++k)
+        if ((1ull << k) == p.m) c.m_shift = k;
     return c;
 }
 

@@ -36,6 +36,7 @@ __host__ __device__ inline uint64_t chunk_hi(uint64_t edge, uint32_t d1) { retur
 struct CostParams {
     uint64_t d1, d2, m, mr;
     uint64_t an, ad, bn, bd, gn, gd;
+    int m_shift;                 // log2(m) when m is a power of two, else -1
 };
 
 // Section 5.1 engine selection, evaluated identically on host (tests) and device.

@@ -45,7 +45,6 @@ __device__ __forceinline__ void write_tiles(uint32_t *tile, uint64_t pre, uint64
 template <bool PR>
 __global__ void __launch_bounds__(kItemThreads) k_plan_items(PlanArgs A) {
     __shared__ uint64_t sh[33];
-    __shared__ double shd[32];
     __shared__ bool is_last;
     const DevState &s = A.s;
     const uint64_t item = A.item_lo + blockIdx.x;
@@ -59,6 +58,7 @@ __global__ void __launch_bounds__(kItemThreads) k_plan_items(PlanArgs A) {
     if (ws + lane < w1) myword = s.bm_cur[ws + lane] & range_mask(ws + lane, vlo, vhi);
     uint64_t e = 0, a = 0, z = 0, ent = 0, ch = 0, hub = 0;
     double ds = 0.0;
+    const int ms = A.cp.m_shift;     // m = 2^ms (the default 128) -> no 64-bit division
     for (uint32_t m = __ballot_sync(FULL_MASK, myword != 0); m; m &= m - 1) {
         const int j = __ffs(m) - 1;
         const uint32_t bits = __shfl_sync(FULL_MASK, myword, j);
@@ -70,19 +70,38 @@ __global__ void __launch_bounds__(kItemThreads) k_plan_items(PlanArgs A) {
             if (deg) {
                 ent += 1;
                 ch += chunk_hi(o1, d1) - chunk_lo(o0, d1);
-                z += zc_lines(o0 * d1, deg * d1, A.cp.m);
+                const uint64_t st = o0 * d1, en = o1 * d1 - 1;
+                z += ms >= 0 ? (en >> ms) - (st >> ms) + 1 : zc_lines(st, deg * d1, A.cp.m);
                 hub += deg * (uint64_t)s.din[v];
             }
             if (PR) ds += (double)s.delta[v];
         }
     }
-    e = block_sum_u64(e, sh);
-    a = block_sum_u64(a, sh);
-    z = block_sum_u64(z, sh);
-    ent = block_sum_u64(ent, sh);
-    ch = block_sum_u64(ch, sh);
-    hub = block_sum_u64(hub, sh);
-    if (PR) ds = block_sum_f64(ds, shd);
+    // one reduction pass for all seven aggregates
+    {
+        __shared__ uint64_t sred[6][kItemThreads / 32];
+        __shared__ double sdred[kItemThreads / 32];
+        uint64_t vals[6] = {e, a, z, ent, ch, hub};
+#pragma unroll
+        for (int f = 0; f < 6; ++f) vals[f] = warp_sum_u64(vals[f]);
+        if (PR) ds = warp_sum_f64(ds);
+        if (lane == 0) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f) sred[f][warp] = vals[f];
+            sdred[warp] = ds;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t t[6] = {0, 0, 0, 0, 0, 0};
+            double td = 0.0;
+            for (int k = 0; k < kItemThreads / 32; ++k) {
+#pragma unroll
+                for (int f = 0; f < 6; ++f) t[f] += sred[f][k];
+                td += sdred[k];
+            }
+            e = t[0]; a = t[1]; z = t[2]; ent = t[3]; ch = t[4]; hub = t[5]; ds = td;
+        }
+    }
     if (threadIdx.x == 0) {
         ItemAgg g;
         g.e = e; g.a = a; g.z = z; g.ent = ent; g.chunks = ch; g.hub = hub; g.dsum = ds;

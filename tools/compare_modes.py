@@ -29,7 +29,7 @@ def main():
     ap.add_argument("--shift", type=int, default=0)
     ap.add_argument("--budgets", default="16,4")
     ap.add_argument("--algos", default="sssp,pr")
-    ap.add_argument("--modes", default="hybrid,filter,compaction,zerocopy")
+    ap.add_argument("--modes", default="hybrid,filter,compaction,zerocopy,hybrid+cache")
     ap.add_argument("--runs", type=int, default=2)
     ap.add_argument("--out", default="gpurun_out/modes.json")
     a = ap.parse_args()
@@ -50,7 +50,8 @@ def main():
             for mode in a.modes.split(","):
                 row = {"budget_gb": b, "algo": algo, "mode": mode}
                 try:
-                    G.set("engine_mode", mode)
+                    G.set("edge_cache", 1 if mode.endswith("+cache") else 0)
+                    G.set("engine_mode", mode.replace("+cache", ""))
                     G.run(algo, 0)                 # warm-up (builds the run context)
                     vals = G.values()
                     edges = int(deg[vals != 0xFFFFFFFF].sum()) if algo in ("sssp", "bfs") else g.E
