@@ -88,6 +88,9 @@ __device__ __forceinline__ uint32_t ld_keep(const uint32_t *p, uint64_t pol) {
     asm volatile("ld.global.cg.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
     return r;
 }
+__device__ __forceinline__ void red_min_keep(uint32_t *p, uint32_t x, uint64_t pol) {
+    asm volatile("red.global.min.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(x), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void red_add_keep(float *p, float x, uint64_t pol) {
     asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(x), "l"(pol) : "memory");
 }
@@ -224,15 +227,24 @@ k_relax(RelaxArgs A) {
                             cur[rr][qd] = ok ? ld_keep(&S.val[d], pol_keep) : 0u;
                         }
                     }
+                    // issue every improving atomicMin first (their round trips overlap),
+                    // then mark the vertices whose value this lane actually lowered.  The
+                    // mark depends on the returned value, so it is ordered after the
+                    // min: the recompute pass's clear-then-read protocol stays sound.
+                    uint32_t old[2][EPC];
 #pragma unroll
                     for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
                         for (int qd = 0; qd < EPC; ++qd) {
-                            const uint32_t d = dst[rr][qd], cnd = cand[rr][qd];
-                            if (cnd < cur[rr][qd]) {
-                                const uint32_t old = atomicMin(&S.val[d], cnd);
-                                if (cnd < old) atomicOr(&S.bm_next[d >> 5], 1u << (d & 31));
-                            }
+                            old[rr][qd] = 0u;          // "not issued": never marks
+                            if (cand[rr][qd] < cur[rr][qd]) old[rr][qd] = atomicMin(&S.val[dst[rr][qd]], cand[rr][qd]);
+                        }
+#pragma unroll
+                    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+                        for (int qd = 0; qd < EPC; ++qd) {
+                            const uint32_t d = dst[rr][qd];
+                            if (cand[rr][qd] < old[rr][qd]) atomicOr(&S.bm_next[d >> 5], 1u << (d & 31));
                         }
                 }
             }

@@ -5,6 +5,8 @@
 // caller's edge arrays are read in place through a temporary host mapping.
 #include <cub/cub.cuh>
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <sys/mman.h>
@@ -118,40 +120,57 @@ __global__ void k_finish_perm(uint64_t V, uint64_t h, const uint32_t *__restrict
     if (blockIdx.x == 0 && threadIdx.x == 0) deg2[V] = 0;
 }
 
-// warp per new row (rows of degree <= big); weights travel with their edge.
-__global__ void k_relabel_rows(uint64_t V, const uint64_t *__restrict__ off_old, const uint64_t *__restrict__ off_new,
-                               const uint32_t *__restrict__ old_of, const uint32_t *__restrict__ new_id,
-                               const uint32_t *__restrict__ nbr_in, const uint32_t *__restrict__ w_in,
-                               uint32_t *__restrict__ nbr_out, uint64_t *__restrict__ ew_out, uint64_t big) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t r = warp; r < V; r += nwarps) {
-        const uint64_t d = off_new[r], deg = off_new[r + 1] - d;
-        if (deg == 0 || deg > big) continue;
-        const uint64_t s = off_old[old_of[r]];
-        for (uint64_t j = lane; j < deg; j += 32) {
-            const uint32_t y = new_id[nbr_in[s + j]];
-            nbr_out[d + j] = y;
-            if (ew_out) ew_out[d + j] = (uint64_t)y | ((uint64_t)w_in[s + j] << 32);
-        }
-    }
-}
+// Relabelled copy of the edges, edge-parallel: a CTA takes a tile of 8192 new edge
+// slots; the rows overlapping it are staged in shared memory (new start, old start)
+// and each thread finds its row by binary search, then copies id (mapped through
+// new_id) and weight.  Reads of the caller's arrays and writes of the pinned store
+// are both coalesced (consecutive slots of a row are consecutive on both sides).
+constexpr int kRelabelTile = 8192, kRelabelRows = 2048;
 
-// CTA per (big row, slice) work item.
-__global__ void k_relabel_big(const uint64_t *__restrict__ items, uint64_t slice, const uint64_t *__restrict__ off_old,
-                              const uint64_t *__restrict__ off_new, const uint32_t *__restrict__ old_of,
-                              const uint32_t *__restrict__ new_id, const uint32_t *__restrict__ nbr_in,
-                              const uint32_t *__restrict__ w_in, uint32_t *__restrict__ nbr_out,
-                              uint64_t *__restrict__ ew_out) {
-    const uint64_t r = items[2 * blockIdx.x], sl = items[2 * blockIdx.x + 1];
-    const uint64_t d = off_new[r], deg = off_new[r + 1] - d;
-    const uint64_t s = off_old[old_of[r]];
-    const uint64_t j0 = sl * slice, j1 = min(deg, j0 + slice);
-    for (uint64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
-        const uint32_t y = new_id[nbr_in[s + j]];
-        nbr_out[d + j] = y;
-        if (ew_out) ew_out[d + j] = (uint64_t)y | ((uint64_t)w_in[s + j] << 32);
+__global__ void __launch_bounds__(512)
+k_relabel_tiles(uint64_t V, uint64_t E, const uint64_t *__restrict__ off_old, const uint64_t *__restrict__ off_new,
+                const uint32_t *__restrict__ old_of, const uint32_t *__restrict__ new_id,
+                const uint32_t *__restrict__ nbr_in, const uint32_t *__restrict__ w_in,
+                uint32_t *__restrict__ nbr_out, uint64_t *__restrict__ ew_out) {
+    __shared__ uint64_t s_new[kRelabelRows + 1];
+    __shared__ uint64_t s_old[kRelabelRows];
+    __shared__ uint64_t s_r0;
+    const uint64_t ntiles = (E + kRelabelTile - 1) / kRelabelTile;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        uint64_t e = t * kRelabelTile;
+        const uint64_t e_end = min(E, e + kRelabelTile);
+        while (e < e_end) {
+            __syncthreads();
+            if (threadIdx.x == 0) {        // last row whose start <= e (skips empty rows)
+                uint64_t lo = 0, hi = V - 1;
+                while (lo < hi) {
+                    const uint64_t mid = (lo + hi + 1) / 2;
+                    if (off_new[mid] <= e) lo = mid; else hi = mid - 1;
+                }
+                s_r0 = lo;
+            }
+            __syncthreads();
+            const uint64_t r0 = s_r0;
+            const uint64_t nr = min((uint64_t)kRelabelRows, V - r0);
+            for (uint64_t i = threadIdx.x; i <= nr; i += blockDim.x) {
+                s_new[i] = off_new[r0 + i];
+                if (i < nr) s_old[i] = off_old[old_of[r0 + i]];
+            }
+            __syncthreads();
+            const uint64_t stop = min(e_end, s_new[nr]);   // edges the staged rows cover
+            for (uint64_t x = e + threadIdx.x; x < stop; x += blockDim.x) {
+                int lo = 0, hi = (int)nr - 1;              // last staged row starting <= x
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (s_new[mid] <= x) lo = mid; else hi = mid - 1;
+                }
+                const uint64_t src = s_old[lo] + (x - s_new[lo]);
+                const uint32_t y = new_id[nbr_in[src]];
+                nbr_out[x] = y;
+                if (ew_out) ew_out[x] = (uint64_t)y | ((uint64_t)w_in[src] << 32);
+            }
+            e = stop;
+        }
     }
 }
 
@@ -222,8 +241,21 @@ struct HostView {
 // ---------------------------------------------------------------------------
 // load
 // ---------------------------------------------------------------------------
+static double wall_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const uint32_t *nbr,
                 const uint32_t *w, uint32_t flags) {
+    const bool verbose = getenv("HYT_VERBOSE") != nullptr;
+    double tph = wall_ms();
+    auto phase = [&](const char *name) {
+        if (!verbose) return;
+        cudaStreamSynchronize(g->main);
+        const double t = wall_ms();
+        fprintf(stderr, "[hyt load] %-28s %8.1f ms\n", name, t - tph);
+        tph = t;
+    };
     HYT_REQUIRE(!g->loaded, HYT_ESTATE, "graph already loaded");
     HYT_REQUIRE(V > 0 && V < (1ull << 32), HYT_EINVAL, "V must be in [1, 2^32)");
     HYT_REQUIRE(off != nullptr && (E == 0 || nbr != nullptr), HYT_EINVAL, "null CSR array");
@@ -255,15 +287,18 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
     HYT_CUDA(cudaMemsetAsync(din, 0, V * 4, st));
     HYT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
 
+    phase("validate + device alloc");
     HostView vn, vw;
     try {
         vn.open(nbr, E * 4);
         if (w) vw.open(w, E * 4);
+        phase("map caller arrays");
         if (E) k_indeg<<<grid_for(E), 256, 0, st>>>((const uint32_t *)vn.dev, E, V, din, bad);
         uint32_t bad_h = 0;
         HYT_CUDA(cudaMemcpyAsync(&bad_h, bad, 4, cudaMemcpyDeviceToHost, st));
         HYT_CUDA(cudaStreamSynchronize(st));
         HYT_REQUIRE(bad_h == 0, HYT_EINVAL, "neighbour id >= V");
+        phase("in-degrees (zero-copy)");
 
         // ---- hub sort: top h = ceil(frac*V) by D_o*D_i ----
         const uint64_t fden = 1000000;
@@ -295,6 +330,7 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         HYT_CUDA(cub::DeviceScan::ExclusiveSum(tscan2, t2, deg2, g->off_d, (int)(V + 1), st));
         g->off_h.resize(V + 1);
         HYT_CUDA(cudaMemcpyAsync(g->off_h.data(), g->off_d, (V + 1) * 8, cudaMemcpyDeviceToHost, st));
+        phase("hub sort + new offsets");
 
         // ---- pinned mapped edge store (16-B padded so chunk loads never overrun) ----
         const uint64_t nbytes = ((E * 4 + 15) & ~15ull) + 32;
@@ -308,28 +344,16 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         HYT_CUDA(cudaHostGetDevicePointer((void **)&nbr_out, g->nbr_h, 0));
         if (w) HYT_CUDA(cudaHostGetDevicePointer((void **)&ew_out, g->ew_h, 0));
         HYT_CUDA(cudaStreamSynchronize(st));   // off_h ready
+        phase("pin edge store");
 
-        const uint64_t big = 8192, slice = 65536;
-        std::vector<uint64_t> items;
-        for (uint64_t r = 0; r < V; ++r) {
-            const uint64_t deg = g->off_h[r + 1] - g->off_h[r];
-            if (deg > big)
-                for (uint64_t sl = 0; sl * slice < deg; ++sl) { items.push_back(r); items.push_back(sl); }
-        }
         if (E) {
-            k_relabel_rows<<<148 * 16, 256, 0, st>>>(V, off_old, g->off_d, g->old_of_d, g->new_id_d,
-                                                     (const uint32_t *)vn.dev, (const uint32_t *)vw.dev,
-                                                     nbr_out, ew_out, big);
-            if (!items.empty()) {
-                uint64_t *items_d = (uint64_t *)T(items.size() * 8, "load: big rows");
-                HYT_CUDA(cudaMemcpyAsync(items_d, items.data(), items.size() * 8, cudaMemcpyHostToDevice, st));
-                k_relabel_big<<<(unsigned)(items.size() / 2), 512, 0, st>>>(
-                    items_d, slice, off_old, g->off_d, g->old_of_d, g->new_id_d, (const uint32_t *)vn.dev,
-                    (const uint32_t *)vw.dev, nbr_out, ew_out);
-            }
+            k_relabel_tiles<<<148 * 4, 512, 0, st>>>(V, E, off_old, g->off_d, g->old_of_d, g->new_id_d,
+                                                      (const uint32_t *)vn.dev, (const uint32_t *)vw.dev, nbr_out,
+                                                      ew_out);
         }
         HYT_CUDA(cudaStreamSynchronize(st));
         HYT_CUDA(cudaGetLastError());
+        phase("relabel edges (zero-copy)");
     } catch (...) {
         cudaStreamSynchronize(st);
         vn.close(); vw.close();
@@ -338,6 +362,7 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
     }
     vn.close(); vw.close();
     for (auto it = tmp.rbegin(); it != tmp.rend(); ++it) A.release(*it);
+    phase("unmap + release");
     g->loaded = true;
 }
 
