@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-shift", type=int, default=6, help="oracle sample = the workload >> cpu_shift")
     ap.add_argument("--json-out", default="")
     ap.add_argument("--detail-out", default="", help="write per-iteration logs + stats of the last step here")
+    ap.add_argument("--set", action="append", default=[], help="extra library parameter key=value (experiments)")
     return ap.parse_args()
 
 
@@ -108,6 +109,14 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------------- workload
+
+def workload_desc(config: str, shift: int, algos) -> str:
+    import hytgen
+    c = hytgen.scaled(config, shift) if shift else hytgen.CONFIGS[config]
+    kind = "undirected (symmetrised)" if c["symmetric"] else "directed"
+    return (f"{config}" + (f">>{shift}" if shift else "") + f": RMAT {c['V']} V / {c['E']} E {kind}, "
+            "u32 weights 1..63; " + "+".join(algos) + " from vertex 0 (PR eps 1e-6)")
+
 
 def make_graph(config: str, shift: int, weighted: bool):
     import hytgen
@@ -211,8 +220,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": val, "unit": "GTEPS", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"{args.config} SSSP+PR (oracle sample {args.config}>>{shift})",
-                       "algos": algos},
+            "config": {"workload": workload_desc(args.config, args.shift, algos), "budget_gb": args.budget_gb,
+                       "engine_mode": args.engine, "reference_sample": f"{args.config}>>{shift}"},
             "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -251,6 +260,9 @@ def main():
             dist.broadcast_object_list(uid, src=0)
             G.init_dist(rank, world, uid[0])
         G.set("engine_mode", args.engine)
+        for kv in args.set:
+            k, v = kv.split("=")
+            G.set(k, float(v))
         return G
 
     G = new_handle()
@@ -416,10 +428,9 @@ def main():
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32(sssp)+f32(pr)", "data": "synthetic",
-        "config": {"workload": f"{args.config}" + (f">>{args.shift}" if args.shift else "") +
-                   f": RMAT {g.V} V / {g.E} E directed, u32 weights 1..63; " + "+".join(algos) +
-                   " from vertex 0 (PR eps 1e-6)",
+        "config": {"workload": workload_desc(args.config, args.shift, algos),
                    "budget_gb": args.budget_gb, "engine_mode": args.engine, "partition_bytes": 32 << 20,
+                   "params": args.set,
                    "parallelism": f"vertex-range x{world}" if world > 1 else "single GPU",
                    "l2": L2_NOTE, "degree_stats": dstats},
         "per_algo": per_algo,

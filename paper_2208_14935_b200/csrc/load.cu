@@ -77,13 +77,51 @@ __global__ void k_indeg(const uint32_t *__restrict__ nbr, uint64_t E, uint64_t V
 
 // H(v) = D_o D_i / (D_omax D_imax): the denominator is common, so the exact
 // integer key D_o*D_i orders the vertices as H does.
-__global__ void k_hub_keys(const uint64_t *__restrict__ off, const uint32_t *__restrict__ din, uint64_t V,
-                           uint64_t *__restrict__ key, uint32_t *__restrict__ ids) {
+__device__ __forceinline__ uint64_t hub_key(const uint64_t *off, const uint32_t *din, uint64_t v) {
+    return (off[v + 1] - off[v]) * (uint64_t)din[v];
+}
+
+// radix select, one 8-bit digit per pass: histogram of the digit at `shift` among
+// keys whose higher bits equal `prefix` (under `mask`)
+__global__ void k_key_hist(const uint64_t *__restrict__ off, const uint32_t *__restrict__ din, uint64_t V,
+                           uint64_t prefix, uint64_t mask, int shift, unsigned long long *__restrict__ hist) {
+    __shared__ unsigned int sh[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
-        key[v] = (off[v + 1] - off[v]) * (uint64_t)din[v];
-        ids[v] = (uint32_t)v;
+        const uint64_t k = hub_key(off, din, v);
+        if ((k & mask) == prefix) atomicAdd(&sh[(k >> shift) & 0xFF], 1u);
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], (unsigned long long)sh[i]);
+}
+
+__global__ void k_tie_flags(const uint64_t *__restrict__ off, const uint32_t *__restrict__ din, uint64_t V,
+                            uint64_t T, uint32_t *__restrict__ flag) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride)
+        flag[v] = hub_key(off, din, v) == T;
+}
+
+// hub iff key > T, or key == T and among the first `ties` such vertices by id
+__global__ void k_hub_flags(const uint64_t *__restrict__ off, const uint32_t *__restrict__ din, uint64_t V,
+                            uint64_t T, uint64_t ties, const uint32_t *__restrict__ tie_rank,
+                            uint32_t *__restrict__ flag) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
+        const uint64_t k = hub_key(off, din, v);
+        flag[v] = k > T || (k == T && tie_rank[v] < ties);
+    }
+}
+
+__global__ void k_scatter_hubs(const uint64_t *__restrict__ off, const uint32_t *__restrict__ din, uint64_t V,
+                               const uint32_t *__restrict__ flag, const uint32_t *__restrict__ pos,
+                               uint32_t *__restrict__ hub_ids, uint64_t *__restrict__ hub_keys) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride)
+        if (flag[v]) { hub_ids[pos[v]] = (uint32_t)v; hub_keys[pos[v]] = hub_key(off, din, v); }
 }
 
 __global__ void k_mark_hubs(const uint32_t *__restrict__ sorted_ids, uint64_t h, uint32_t *__restrict__ new_id,
@@ -280,7 +318,6 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
     uint64_t *off_old = (uint64_t *)T((V + 1) * 8, "load: caller offsets");
     uint32_t *din = (uint32_t *)T(V * 4 + 16, "load: in-degree");
     uint32_t *bad = (uint32_t *)T(16, "load: flag");
-    uint64_t *deg2 = (uint64_t *)T((V + 1) * 8, "load: degrees");
     uint32_t *nonhub = (uint32_t *)T(V * 4 + 16, "load: non-hub flags");
     uint32_t *nonhub_scan = (uint32_t *)T(V * 4 + 16, "load: non-hub scan");
     HYT_CUDA(cudaMemcpyAsync(off_old, off, (V + 1) * 8, cudaMemcpyHostToDevice, st));
@@ -307,17 +344,54 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         if (h > V) h = V;
         k_fill_u32<<<grid_for(V), 256, 0, st>>>(nonhub, V, 1u);
         if (h > 0) {
-            uint64_t *key = (uint64_t *)T(V * 8, "load: hub keys");
-            uint64_t *key2 = (uint64_t *)T(V * 8, "load: hub keys sorted");
-            uint32_t *ids = (uint32_t *)T(V * 4 + 16, "load: ids");
-            uint32_t *ids2 = (uint32_t *)T(V * 4 + 16, "load: ids sorted");
-            k_hub_keys<<<grid_for(V), 256, 0, st>>>(off_old, din, V, key, ids);
+            // exact radix select of the h-th largest key T (8 passes of 8 bits), then
+            // only the h hubs are sorted: O(V) memory instead of a full-V key sort
+            unsigned long long *hist = (unsigned long long *)T(256 * 8, "load: select histogram");
+            std::vector<unsigned long long> hh(256);
+            uint64_t prefix = 0, mask = 0, kk = h;
+            for (int pass = 0; pass < 8; ++pass) {
+                const int shift = 56 - 8 * pass;
+                HYT_CUDA(cudaMemsetAsync(hist, 0, 256 * 8, st));
+                k_key_hist<<<grid_for(V, 256, 148 * 8), 256, 0, st>>>(off_old, din, V, prefix, mask, shift, hist);
+                HYT_CUDA(cudaMemcpyAsync(hh.data(), hist, 256 * 8, cudaMemcpyDeviceToHost, st));
+                HYT_CUDA(cudaStreamSynchronize(st));
+                unsigned long long acc = 0;
+                int d = 255;
+                for (; d > 0; --d) {
+                    if (acc + hh[d] >= kk) break;
+                    acc += hh[d];
+                }
+                kk -= acc;
+                prefix |= (uint64_t)d << shift;
+                mask |= 0xFFull << shift;
+            }
+            const uint64_t Tkey = prefix, ties = kk;      // hubs: key > T, plus `ties` of key == T by id
+            k_tie_flags<<<grid_for(V), 256, 0, st>>>(off_old, din, V, Tkey, nonhub);
+            size_t t0 = 0;
+            HYT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t0, nonhub, nonhub_scan, (int)V, st));
+            void *tsc = T(t0 + 16, "load: select scan temp");
+            HYT_CUDA(cub::DeviceScan::ExclusiveSum(tsc, t0, nonhub, nonhub_scan, (int)V, st));
+            k_hub_flags<<<grid_for(V), 256, 0, st>>>(off_old, din, V, Tkey, ties, nonhub_scan, nonhub);
+            HYT_CUDA(cub::DeviceScan::ExclusiveSum(tsc, t0, nonhub, nonhub_scan, (int)V, st));
+            uint32_t *hid = (uint32_t *)T(h * 4 + 16, "load: hub ids");
+            uint32_t *hid2 = (uint32_t *)T(h * 4 + 16, "load: hub ids sorted");
+            uint64_t *hkey = (uint64_t *)T(h * 8 + 16, "load: hub keys");
+            uint64_t *hkey2 = (uint64_t *)T(h * 8 + 16, "load: hub keys sorted");
+            k_scatter_hubs<<<grid_for(V), 256, 0, st>>>(off_old, din, V, nonhub, nonhub_scan, hid, hkey);
             size_t tb = 0;
-            HYT_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, key, key2, ids, ids2, (int)V, 0, 64, st));
-            void *tsort = T(tb + 16, "load: sort temp");
-            HYT_CUDA(cub::DeviceRadixSort::SortPairsDescending(tsort, tb, key, key2, ids, ids2, (int)V, 0, 64, st));
-            k_mark_hubs<<<grid_for(h), 256, 0, st>>>(ids2, h, g->new_id_d, nonhub);
+            HYT_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, hkey, hkey2, hid, hid2, (int)h, 0, 64, st));
+            void *tsort = T(tb + 16, "load: hub sort temp");
+            // stable: equal keys keep ascending ids
+            HYT_CUDA(cub::DeviceRadixSort::SortPairsDescending(tsort, tb, hkey, hkey2, hid, hid2, (int)h, 0, 64, st));
+            k_fill_u32<<<grid_for(V), 256, 0, st>>>(nonhub, V, 1u);
+            k_mark_hubs<<<grid_for(h), 256, 0, st>>>(hid2, h, g->new_id_d, nonhub);
+            HYT_CUDA(cudaStreamSynchronize(st));
+            for (void *q : {(void *)tsort, (void *)hkey2, (void *)hkey, (void *)hid2, (void *)hid, tsc, (void *)hist}) {
+                A.release(q);
+                tmp.erase(std::find(tmp.begin(), tmp.end(), q));
+            }
         }
+        uint64_t *deg2 = (uint64_t *)T((V + 1) * 8, "load: degrees");
         size_t ts = 0;
         HYT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, ts, nonhub, nonhub_scan, (int)V, st));
         void *tscan = T(ts + 16, "load: scan temp");
