@@ -24,7 +24,15 @@ hytgen/libhytgen.so: hytgen/hytgen.c
 oracle/liboracle.so: oracle/oracle.c
 	gcc -O2 -fPIC -shared -o $@ $< -lm
 
+tools: tools/pin_bench tools/zc_bench
+
+tools/pin_bench: tools/pin_bench.cu
+	$(NVCC) $(ARCH) -O2 -o $@ $< -lpthread
+
+tools/zc_bench: tools/zc_bench.cu
+	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
+
 clean:
 	rm -rf build $(LIB) hytgen/libhytgen.so oracle/liboracle.so
 
-.PHONY: all clean
+.PHONY: all clean tools

@@ -158,7 +158,11 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   the budget left after the run buffers resident in device memory (served as
  *   engine R at no transfer cost, beyond the paper, whose edges
  *   are re-transferred every iteration); edge_cache_bytes [0 = no cap]
- *   caps its size.
+ *   caps its size; cpu_cost [0]: 1 adds Eq. 2's CPU-gather term
+ *   (bytes / Thpt_cpt) to the compaction cost in selection, with the
+ *   link rate and Thpt_cpt calibrated on this box (or set by link_gbs /
+ *   thpt_cpt_gbs); the paper omits the term in selection, so 0 is the
+ *   paper's rule.
  * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
 int hyt_set_param(hyt_graph *g, const char *key, double value);
 

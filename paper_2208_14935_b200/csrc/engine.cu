@@ -78,7 +78,7 @@ void Arena::release_all() {
     ext_top = 0;
 }
 
-CostParams make_cost(const Params &p, uint32_t d1) {
+CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio) {
     CostParams c;
     c.d1 = d1; c.d2 = p.d2; c.m = p.m; c.mr = p.mr;
     const uint64_t den = 1000000;
@@ -88,6 +88,8 @@ CostParams make_cost(const Params &p, uint32_t d1) {
     c.m_shift = -1;
     for (int k = 0; k < 63; ++k)
         if ((1ull << k) == p.m) c.m_shift = k;
+    c.cd = 1000;
+    c.cn = cpu_ratio > 0 ? (uint64_t)(cpu_ratio * 1000 + 0.5) : 0;
     return c;
 }
 
@@ -560,8 +562,8 @@ static DevState make_state(hyt_graph *g, RunCtx *c) {
 // ---------------------------------------------------------------------------
 // compaction gather: chunks [w_lo, w_hi) of the C segment into dst (host)
 // ---------------------------------------------------------------------------
-static void gather_window(RunCtx *c, const uint4 *edges_host, const std::vector<uint64_t> &off, uint64_t n,
-                          uint64_t w_lo, uint64_t w_hi, uint4 *dst) {
+void gather_window(RunCtx *c, const uint4 *edges_host, const std::vector<uint64_t> &off, uint64_t n,
+                   uint64_t w_lo, uint64_t w_hi, uint4 *dst) {
     // first entry covering w_lo
     const uint64_t *pre = c->cq_pre;
     uint64_t k0 = std::upper_bound(pre, pre + n, w_lo) - pre - 1;
@@ -580,6 +582,68 @@ static void gather_window(RunCtx *c, const uint4 *edges_host, const std::vector<
     });
 }
 
+static inline double now_ms();
+
+// Calibrate the Eq. 2 CPU term on this box: the H2D link rate
+// (one timed 256 MiB copy from the pinned store) and the host gather throughput
+// Thpt_cpt (the compaction workers gathering the lists of random vertices).
+static void calibrate_cpu_cost(hyt_graph *g, RunCtx *c) {
+    const Params &P = g->prm;
+    if (!P.cpu_cost) return;
+    if (P.link_gbs > 0) g->est_link_gbs = P.link_gbs;
+    if (P.thpt_cpt_gbs > 0) g->est_cpt_gbs = P.thpt_cpt_gbs;
+    const uint4 *edges_host = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
+    const uint64_t total16 = chunk_hi(g->E, c->d1);
+    if (g->est_link_gbs <= 0 && !c->slot.empty() && total16) {
+        const uint64_t bytes = std::min<uint64_t>(c->slot_bytes, std::min<uint64_t>(256ull << 20, total16 * 16));
+        cudaEvent_t a, b;
+        HYT_CUDA(cudaEventCreate(&a));
+        HYT_CUDA(cudaEventCreate(&b));
+        HYT_CUDA(cudaMemcpyAsync(c->slot[0], edges_host, bytes, cudaMemcpyHostToDevice, g->main));
+        HYT_CUDA(cudaEventRecord(a, g->main));
+        HYT_CUDA(cudaMemcpyAsync(c->slot[0], edges_host, bytes, cudaMemcpyHostToDevice, g->main));
+        HYT_CUDA(cudaEventRecord(b, g->main));
+        HYT_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        HYT_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        g->est_link_gbs = bytes / (ms / 1e3) / 1e9;
+    }
+    if (g->est_cpt_gbs <= 0 && c->pool && c->cq_cap > 1) {
+        // the lists of up to 64K random vertices with out-edges, gathered like the C engine
+        std::vector<uint32_t> vs;
+        uint64_t x = 0x9E3779B97F4A7C15ull;
+        for (uint64_t tries = 0; vs.size() < 65536 && tries < 1000000; ++tries) {
+            x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+            const uint64_t v = x % g->V;
+            if (g->off_h[v + 1] > g->off_h[v]) vs.push_back((uint32_t)v);
+        }
+        const uint64_t n = std::min<uint64_t>(vs.size(), c->cq_cap);
+        uint64_t pre = 0;
+        for (uint64_t k = 0; k < n; ++k) {
+            c->cq_v[k] = vs[k];
+            c->cq_pre[k] = pre;
+            pre += chunk_hi(g->off_h[vs[k] + 1], c->d1) - chunk_lo(g->off_h[vs[k]], c->d1);
+        }
+        const uint64_t w_hi = std::min<uint64_t>(pre, c->cbuf_bytes / 16);
+        if (w_hi) {
+            void gather_window(RunCtx *, const uint4 *, const std::vector<uint64_t> &, uint64_t, uint64_t, uint64_t, uint4 *);
+            gather_window(c, edges_host, g->off_h, n, 0, w_hi, c->hstage[0]);   // warm
+            const double t0 = now_ms();
+            gather_window(c, edges_host, g->off_h, n, 0, w_hi, c->hstage[0]);
+            const double ms = now_ms() - t0;
+            g->est_cpt_gbs = w_hi * 16 / (ms / 1e3) / 1e9;
+        }
+    }
+}
+
+static CostParams cost_for(hyt_graph *g, uint32_t d1) {
+    double ratio = 0.0;
+    if (g->prm.cpu_cost && g->est_link_gbs > 0 && g->est_cpt_gbs > 0) ratio = g->est_link_gbs / g->est_cpt_gbs;
+    return make_cost(g->prm, d1, ratio);
+}
+
 static inline double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -595,7 +659,8 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     RunCtx *c = get_ctx(g, algo);
     DevState s = make_state(g, c);
     cudaStream_t main = g->main;
-    const CostParams cp = make_cost(P, c->d1);
+    calibrate_cpu_cost(g, c);
+    const CostParams cp = cost_for(g, c->d1);
     const int mode = P.engine_mode;
     const int prio = P.priority >= 0 ? P.priority : (algo == ALGO_PR ? 2 : 1);
     const int sms = 148;
@@ -793,7 +858,12 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 if (b >= 2) HYT_CUDA(cudaEventSynchronize(c->ev_cbuf[bi]));
                 const double tg = now_ms();
                 gather_window(c, edges_host, g->off_h, nC, w_lo, w_hi, c->hstage[bi]);
-                g->stats.gather_ms += now_ms() - tg;
+                const double gms = now_ms() - tg;
+                g->stats.gather_ms += gms;
+                if (P.cpu_cost && P.thpt_cpt_gbs <= 0 && gms > 0.5) {   // keep Thpt_cpt current (EMA)
+                    const double r = (w_hi - w_lo) * 16 / (gms / 1e3) / 1e9;
+                    g->est_cpt_gbs = g->est_cpt_gbs > 0 ? 0.5 * g->est_cpt_gbs + 0.5 * r : r;
+                }
                 EvPair e1, e2;
                 timed_begin(c, stm, e1, TAG_COPY);
                 HYT_CUDA(cudaMemcpyAsync(c->cbuf[bi], c->hstage[bi], (w_hi - w_lo) * 16, cudaMemcpyHostToDevice, stm));
@@ -933,7 +1003,7 @@ void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_par
     HYT_CUDA(cudaMemsetAsync(c->parts_d, 0, N * sizeof(PartIter), g->main));
     const PlanBufs pb{c->parts_d, c->iagg, c->ibase, c->hdr_d};
     launch_plan(s, c->bounds_d, c->t_d, c->items, 0, c->n_items, 0, N, c->cache_hi, g->prm.engine_mode,
-                make_cost(g->prm, d1), pb, g->main);
+                cost_for(g, d1), pb, g->main);
     std::vector<PartIter> ph(N);
     HYT_CUDA(cudaMemcpyAsync(ph.data(), c->parts_d, N * sizeof(PartIter), cudaMemcpyDeviceToHost, g->main));
     HYT_CUDA(cudaStreamSynchronize(g->main));

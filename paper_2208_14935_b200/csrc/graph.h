@@ -70,9 +70,12 @@ struct Params {
     int relax_ctas_per_sm = 4;
     int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
     uint64_t edge_cache_bytes = 0;   // cap on the cache (0 = whatever the budget leaves)
+    int cpu_cost = 0;          // 1: include Eq. 2's CPU term with Thpt_cpt calibrated on this box
+    double thpt_cpt_gbs = 0;   // host gather throughput (0 = measure)
+    double link_gbs = 0;       // host->device link rate (0 = measure)
 };
 
-CostParams make_cost(const Params &p, uint32_t d1);
+CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio = 0.0);
 
 // Pinned, mapped host memory: mmap + transparent huge pages + parallel first
 // touch + cudaHostRegister.  About 9x faster to create than cudaHostAlloc on the
@@ -120,6 +123,7 @@ struct hyt_graph {
     uint64_t eng_edges[hyt::ENG_COUNT] = {0, 0, 0, 0, 0};
     uint64_t launches = 0;
     void *ctx[4] = {nullptr, nullptr, nullptr, nullptr};   // cached run contexts, one per algorithm
+    double est_link_gbs = 0, est_cpt_gbs = 0;              // calibrated rates (cpu_cost = 1)
     // ---- multi-GPU ----
     int rank = 0, world = 1;
     void *nccl_comm = nullptr;

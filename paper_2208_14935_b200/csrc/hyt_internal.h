@@ -37,6 +37,7 @@ struct CostParams {
     uint64_t d1, d2, m, mr;
     uint64_t an, ad, bn, bd, gn, gd;
     int m_shift;                 // log2(m) when m is a power of two, else -1
+    uint64_t cn, cd;             // Eq. 2 CPU term: link rate / Thpt_cpt as cn/cd (cn = 0: paper practice)
 };
 
 // Section 5.1 engine selection, evaluated identically on host (tests) and device.
@@ -47,7 +48,12 @@ __host__ __device__ inline int select_engine(uint64_t t, uint64_t e, uint64_t a,
     typedef unsigned __int128 u128;
     const uint64_t tlp = c.m * c.mr;
     const uint64_t Tef = (t * c.d1 + tlp - 1) / tlp;                     // Eq. 1
-    const uint64_t Tec = (e * c.d1 + a * c.d2 + tlp - 1) / tlp;          // Eq. 2 (transfer term)
+    uint64_t Tec = (e * c.d1 + a * c.d2 + tlp - 1) / tlp;                // Eq. 2 (transfer term)
+    if (c.cn) {   // + (bytes / Thpt_cpt) in TLP-time units (RTT = m*MR bytes at the link rate)
+        const u128 b = (u128)(e * c.d1 + a * c.d2) * c.cn;
+        const u128 q = (u128)c.cd * tlp;
+        Tec += (uint64_t)((b + q - 1) / q);
+    }
     const uint64_t nz = (z + c.mr - 1) / c.mr;                            // Eq. 3 TLP count
     // Tiz = nz * RTT_zc, RTT_zc = gamma + (1-gamma) e/t  ->  nz*(gn t + (gd-gn) e) / (gd t)
     const u128 num = (u128)nz * ((u128)c.gn * t + (u128)(c.gd - c.gn) * e);

@@ -331,3 +331,22 @@ def test_many_short_lists_large_units(hyt, engine):
             assert np.array_equal(got, oracle.sssp(g.off, g.nbr, g.w, 0))
         else:
             assert np.array_equal(got, oracle.bfs(g.off, g.nbr, 0))
+
+
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "pr"])
+def test_cpu_cost_term(hyt, algo):
+    """cpu_cost=1: Eq. 2's CPU term with Thpt_cpt calibrated on the box
+    changes only which engine serves a partition, never the result."""
+    gkey = ("rmat", 11)
+    g = gkey_graph(gkey)
+    got, st, _ = run_gpu(hyt, g, algo, part=4096, cpu_cost=1)
+    want = expected(gkey, algo)
+    if algo == "pr":
+        assert_pr_close(got, want)
+    else:
+        assert np.array_equal(got, want)
+    # a prohibitively slow host gather removes compaction from the hybrid
+    got, st, _ = run_gpu(hyt, g, algo, part=4096, cpu_cost=1, thpt_cpt_gbs=0.001, link_gbs=50)
+    assert st["parts_compaction"] == 0
+    if algo != "pr":
+        assert np.array_equal(got, want)
