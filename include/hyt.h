@@ -162,7 +162,8 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   (bytes / Thpt_cpt) to the compaction cost in selection, with the
  *   link rate and Thpt_cpt calibrated on this box (or set by link_gbs /
  *   thpt_cpt_gbs); the paper omits the term in selection, so 0 is the
- *   paper's rule.
+ *   paper's rule; zc_weight [1.0] multiplies Tiz (Eq. 3)
+ *   before the comparisons (1 = the paper).
  * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
 int hyt_set_param(hyt_graph *g, const char *key, double value);
 

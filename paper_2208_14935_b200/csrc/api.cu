@@ -109,6 +109,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "edge_cache") { integral(); in(0, 1); p.edge_cache = (int)v; }
         else if (k == "edge_cache_bytes") { integral(); in(0, 1e13); p.edge_cache_bytes = (uint64_t)v; }
         else if (k == "cpu_cost") { integral(); in(0, 1); p.cpu_cost = (int)v; }
+        else if (k == "zc_weight") { in(0.001, 1000); p.zc_weight = v; }
         else if (k == "thpt_cpt_gbs") { in(0, 1e6); p.thpt_cpt_gbs = v; g->est_cpt_gbs = v; }
         else if (k == "link_gbs") { in(0, 1e6); p.link_gbs = v; g->est_link_gbs = v; }
         else throw Err{HYT_EINVAL, "unknown parameter '" + k + "'"};

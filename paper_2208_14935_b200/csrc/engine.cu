@@ -90,6 +90,8 @@ CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio) {
         if ((1ull << k) == p.m) c.m_shift = k;
     c.cd = 1000;
     c.cn = cpu_ratio > 0 ? (uint64_t)(cpu_ratio * 1000 + 0.5) : 0;
+    c.zd = 1000;
+    c.zn = (uint64_t)(p.zc_weight * 1000 + 0.5);
     return c;
 }
 

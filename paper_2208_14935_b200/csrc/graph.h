@@ -73,6 +73,7 @@ struct Params {
     int cpu_cost = 0;          // 1: include Eq. 2's CPU term with Thpt_cpt calibrated on this box
     double thpt_cpt_gbs = 0;   // host gather throughput (0 = measure)
     double link_gbs = 0;       // host->device link rate (0 = measure)
+    double zc_weight = 1.0;    // multiplier on Tiz (1 = the paper's Eq. 3)
 };
 
 CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio = 0.0);

@@ -38,6 +38,7 @@ struct CostParams {
     uint64_t an, ad, bn, bd, gn, gd;
     int m_shift;                 // log2(m) when m is a power of two, else -1
     uint64_t cn, cd;             // Eq. 2 CPU term: link rate / Thpt_cpt as cn/cd (cn = 0: paper practice)
+    uint64_t zn, zd;             // weight on Tiz (zn/zd = 1: the paper's Eq. 3)
 };
 
 // Section 5.1 engine selection, evaluated identically on host (tests) and device.
@@ -56,8 +57,8 @@ __host__ __device__ inline int select_engine(uint64_t t, uint64_t e, uint64_t a,
     }
     const uint64_t nz = (z + c.mr - 1) / c.mr;                            // Eq. 3 TLP count
     // Tiz = nz * RTT_zc, RTT_zc = gamma + (1-gamma) e/t  ->  nz*(gn t + (gd-gn) e) / (gd t)
-    const u128 num = (u128)nz * ((u128)c.gn * t + (u128)(c.gd - c.gn) * e);
-    const u128 den = (u128)c.gd * t;
+    const u128 num = (u128)nz * ((u128)c.gn * t + (u128)(c.gd - c.gn) * e) * c.zn;
+    const u128 den = (u128)c.gd * t * c.zd;
     const bool c1 = (u128)Tec * c.ad < (u128)c.an * Tef;                 // Tec < alpha Tef
     const bool c2 = (u128)Tec * c.bd * den < (u128)c.bn * num;            // Tec < beta Tiz
     if (c1 && c2) return ENG_C;

@@ -50,8 +50,11 @@ def main():
             for mode in a.modes.split(","):
                 row = {"budget_gb": b, "algo": algo, "mode": mode}
                 try:
-                    G.set("edge_cache", 1 if mode.endswith("+cache") else 0)
-                    G.set("engine_mode", mode.replace("+cache", ""))
+                    G.set("edge_cache", 1 if "+cache" in mode else 0)
+                    G.set("cpu_cost", 1 if "+cpu" in mode else 0)
+                    zw = [x for x in mode.split("+") if x.startswith("zw")]
+                    G.set("zc_weight", float(zw[0][2:]) if zw else 1.0)
+                    G.set("engine_mode", mode.split("+")[0])
                     G.run(algo, 0)                 # warm-up (builds the run context)
                     vals = G.values()
                     edges = int(deg[vals != 0xFFFFFFFF].sum()) if algo in ("sssp", "bfs") else g.E

@@ -44,9 +44,13 @@ def main():
     res["load_s"] = time.time() - t
     deg = np.diff(g.off.astype(np.int64))
     for mode in a.modes.split(","):
-        G.set("edge_cache", 1 if mode.endswith("+cache") else 0)
-        G.set("engine_mode", mode.replace("+cache", ""))
+        G.set("edge_cache", 1 if "+cache" in mode else 0)
+        G.set("cpu_cost", 1 if "+cpu" in mode else 0)
+        zw = [x for x in mode.split("+") if x.startswith("zw")]
+        G.set("zc_weight", float(zw[0][2:]) if zw else 1.0)
+        G.set("engine_mode", mode.split("+")[0])
         for algo in algos:
+            G.run(algo, 0)                           # warm-up (run-context build, calibration)
             ms = []
             for _ in range(a.runs):
                 torch.cuda.synchronize()
