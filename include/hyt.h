@@ -100,6 +100,10 @@ typedef struct {
     uint64_t eng_launches[8];
     uint64_t eng_chunks[8];        /* 16-byte edge chunks read by the relax launches */
     uint64_t eng_edges[8];         /* active edges pushed by the relax launches      */
+    /* cost-model calibration on this box (cpu_cost / cost_model = 1; else 0):
+     * DMA link GB/s, host gather GB/s (Thpt_cpt), zero-copy ns per random
+     * 128-B request and per streamed 128-B line. */
+    double   cal_link_gbs, cal_cpt_gbs, cal_zc_req_ns, cal_zc_line_ns;
 } hyt_stats;
 
 /* One row per iteration (hyt_get_iter_log), the Fig. 7 / Table VI analog. */
@@ -163,7 +167,10 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   link rate and Thpt_cpt calibrated on this box (or set by link_gbs /
  *   thpt_cpt_gbs); the paper omits the term in selection, so 0 is the
  *   paper's rule; zc_weight [1.0] multiplies Tiz (Eq. 3)
- *   before the comparisons (1 = the paper).
+ *   before the comparisons (1 = the paper); cost_model [0]: 1 replaces the
+ *   PCIe-3 constants by costs measured on this box -- Eq. 2's CPU term as with
+ *   cpu_cost, and Eq. 3 as (active lists x random-request time + further lines
+ *   x streamed-line time) / RTT, both probed on the mapped edge store.
  * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
 int hyt_set_param(hyt_graph *g, const char *key, double value);
 

@@ -44,7 +44,9 @@ class hyt_stats(ctypes.Structure):
         "units_filter", "device_bytes_peak", "num_partitions")] + [
         (n, ctypes.c_double) for n in ("kernel_ms", "copy_ms", "plan_ms", "gather_ms")] + [
         ("kernel_launches", ctypes.c_uint64), ("eng_ms", ctypes.c_double * 8),
-        ("eng_launches", ctypes.c_uint64 * 8), ("eng_chunks", ctypes.c_uint64 * 8), ("eng_edges", ctypes.c_uint64 * 8)]
+        ("eng_launches", ctypes.c_uint64 * 8), ("eng_chunks", ctypes.c_uint64 * 8), ("eng_edges", ctypes.c_uint64 * 8),
+        ("cal_link_gbs", ctypes.c_double), ("cal_cpt_gbs", ctypes.c_double), ("cal_zc_req_ns", ctypes.c_double),
+        ("cal_zc_line_ns", ctypes.c_double)]
 
 
 class hyt_iter(ctypes.Structure):

@@ -110,6 +110,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "edge_cache_bytes") { integral(); in(0, 1e13); p.edge_cache_bytes = (uint64_t)v; }
         else if (k == "cpu_cost") { integral(); in(0, 1); p.cpu_cost = (int)v; }
         else if (k == "zc_weight") { in(0.001, 1000); p.zc_weight = v; }
+        else if (k == "cost_model") { integral(); in(0, 1); p.cost_model = (int)v; }
         else if (k == "thpt_cpt_gbs") { in(0, 1e6); p.thpt_cpt_gbs = v; g->est_cpt_gbs = v; }
         else if (k == "link_gbs") { in(0, 1e6); p.link_gbs = v; g->est_link_gbs = v; }
         else throw Err{HYT_EINVAL, "unknown parameter '" + k + "'"};
@@ -175,7 +176,7 @@ int hyt_select_engine(const hyt_graph *g, uint64_t t, uint64_t e, uint64_t a, ui
     if (d1 == 0 || d1 > 64) { set_error("bad d1"); return HYT_EINVAL; }
     Params def;
     const Params &p = g ? g->prm : def;
-    return select_engine(t, e, a, z, make_cost(p, (uint32_t)d1));
+    return select_engine(t, e, a, z, a, make_cost(p, (uint32_t)d1));
 }
 
 int64_t hyt_rank_range(const uint64_t *off, uint64_t V, uint64_t d1, uint64_t partition_bytes, int world, int rank,

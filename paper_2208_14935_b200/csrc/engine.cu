@@ -78,7 +78,7 @@ void Arena::release_all() {
     ext_top = 0;
 }
 
-CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio) {
+CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio, double zr_rtt, double zs_rtt) {
     CostParams c;
     c.d1 = d1; c.d2 = p.d2; c.m = p.m; c.mr = p.mr;
     const uint64_t den = 1000000;
@@ -92,6 +92,9 @@ CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio) {
     c.cn = cpu_ratio > 0 ? (uint64_t)(cpu_ratio * 1000 + 0.5) : 0;
     c.zd = 1000;
     c.zn = (uint64_t)(p.zc_weight * 1000 + 0.5);
+    c.zden = 1000000;
+    c.zr = zr_rtt > 0 ? std::max<uint64_t>(1, (uint64_t)(zr_rtt * 1e6 + 0.5)) : 0;
+    c.zs = zs_rtt > 0 ? (uint64_t)(zs_rtt * 1e6 + 0.5) : 0;
     return c;
 }
 
@@ -591,7 +594,7 @@ static inline double now_ms();
 // Thpt_cpt (the compaction workers gathering the lists of random vertices).
 static void calibrate_cpu_cost(hyt_graph *g, RunCtx *c) {
     const Params &P = g->prm;
-    if (!P.cpu_cost) return;
+    if (!P.cpu_cost && !P.cost_model) return;
     if (P.link_gbs > 0) g->est_link_gbs = P.link_gbs;
     if (P.thpt_cpt_gbs > 0) g->est_cpt_gbs = P.thpt_cpt_gbs;
     const uint4 *edges_host = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
@@ -641,9 +644,34 @@ static void calibrate_cpu_cost(hyt_graph *g, RunCtx *c) {
 }
 
 static CostParams cost_for(hyt_graph *g, uint32_t d1) {
-    double ratio = 0.0;
-    if (g->prm.cpu_cost && g->est_link_gbs > 0 && g->est_cpt_gbs > 0) ratio = g->est_link_gbs / g->est_cpt_gbs;
-    return make_cost(g->prm, d1, ratio);
+    const Params &P = g->prm;
+    double ratio = 0.0, zr = 0.0, zs = 0.0;
+    if ((P.cpu_cost || P.cost_model) && g->est_link_gbs > 0 && g->est_cpt_gbs > 0)
+        ratio = g->est_link_gbs / g->est_cpt_gbs;
+    if (P.cost_model && g->est_link_gbs > 0 && g->est_zc_req_ns > 0) {
+        // RTT = the time of one saturated TLP (m * MR bytes) at the DMA link rate
+        const double rtt_ns = (double)(P.m * P.mr) / g->est_link_gbs;
+        zr = g->est_zc_req_ns / rtt_ns;
+        zs = g->est_zc_line_ns / rtt_ns;
+    }
+    return make_cost(P, d1, ratio, zr, zs);
+}
+
+// Zero-copy request costs on this box (cost_model = 1): a random 128-byte line and
+// a streamed line of the mapped edge store (the Fig. 3e measurement).
+static void calibrate_zero_copy(hyt_graph *g, RunCtx *c) {
+    if (!g->prm.cost_model || g->est_zc_req_ns > 0) return;
+    const uint4 *edges_host = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
+    const uint4 *mapped = nullptr;
+    HYT_CUDA(cudaHostGetDevicePointer((void **)&mapped, (void *)edges_host, 0));
+    const uint64_t nlines = chunk_hi(g->E, c->d1) / 8;
+    if (nlines < 1024) return;
+    uint64_t lines = 0;
+    const float ms_r = time_zc_probe(mapped, nlines, 0, (uint32_t *)c->racc, &lines, g->main);
+    g->est_zc_req_ns = ms_r * 1e6 / lines;
+    const float ms_s = time_zc_probe(mapped, nlines, 1, (uint32_t *)c->racc, &lines, g->main);
+    g->est_zc_line_ns = ms_s * 1e6 / lines;
+    HYT_CUDA(cudaGetLastError());
 }
 
 static inline double now_ms() {
@@ -662,6 +690,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     DevState s = make_state(g, c);
     cudaStream_t main = g->main;
     calibrate_cpu_cost(g, c);
+    calibrate_zero_copy(g, c);
     const CostParams cp = cost_for(g, c->d1);
     const int mode = P.engine_mode;
     const int prio = P.priority >= 0 ? P.priority : (algo == ALGO_PR ? 2 : 1);
@@ -862,7 +891,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 gather_window(c, edges_host, g->off_h, nC, w_lo, w_hi, c->hstage[bi]);
                 const double gms = now_ms() - tg;
                 g->stats.gather_ms += gms;
-                if (P.cpu_cost && P.thpt_cpt_gbs <= 0 && gms > 0.5) {   // keep Thpt_cpt current (EMA)
+                if ((P.cpu_cost || P.cost_model) && P.thpt_cpt_gbs <= 0 && gms > 0.5) {   // keep Thpt_cpt current (EMA)
                     const double r = (w_hi - w_lo) * 16 / (gms / 1e3) / 1e9;
                     g->est_cpt_gbs = g->est_cpt_gbs > 0 ? 0.5 * g->est_cpt_gbs + 0.5 * r : r;
                 }
@@ -934,6 +963,10 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     g->stats.copy_ms = g->copy_time.ms;
     g->stats.plan_ms = g->plan_time.ms;
     g->stats.kernel_launches = g->launches;
+    g->stats.cal_link_gbs = g->est_link_gbs;
+    g->stats.cal_cpt_gbs = g->est_cpt_gbs;
+    g->stats.cal_zc_req_ns = g->est_zc_req_ns;
+    g->stats.cal_zc_line_ns = g->est_zc_line_ns;
     for (int i = 0; i < 8; ++i) { g->stats.eng_ms[i] = 0; g->stats.eng_launches[i] = 0; g->stats.eng_chunks[i] = 0; g->stats.eng_edges[i] = 0; }
     g->stats.eng_ms[0] = g->plan_time.ms; g->stats.eng_launches[0] = g->plan_time.launches;
     for (int i = 1; i < ENG_COUNT; ++i) {

@@ -74,9 +74,11 @@ struct Params {
     double thpt_cpt_gbs = 0;   // host gather throughput (0 = measure)
     double link_gbs = 0;       // host->device link rate (0 = measure)
     double zc_weight = 1.0;    // multiplier on Tiz (1 = the paper's Eq. 3)
+    int cost_model = 0;        // 0: the paper's Eq. 1-3 (PCIe-3 constants); 1: calibrated on this box
 };
 
-CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio = 0.0);
+CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio = 0.0, double zr_rtt = 0.0,
+                     double zs_rtt = 0.0);
 
 // Pinned, mapped host memory: mmap + transparent huge pages + parallel first
 // touch + cudaHostRegister.  About 9x faster to create than cudaHostAlloc on the
@@ -125,6 +127,7 @@ struct hyt_graph {
     uint64_t launches = 0;
     void *ctx[4] = {nullptr, nullptr, nullptr, nullptr};   // cached run contexts, one per algorithm
     double est_link_gbs = 0, est_cpt_gbs = 0;              // calibrated rates (cpu_cost = 1)
+    double est_zc_req_ns = 0, est_zc_line_ns = 0;          // zero-copy random request / stream line (cost_model = 1)
     // ---- multi-GPU ----
     int rank = 0, world = 1;
     void *nccl_comm = nullptr;

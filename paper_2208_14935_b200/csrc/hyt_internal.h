@@ -39,11 +39,15 @@ struct CostParams {
     int m_shift;                 // log2(m) when m is a power of two, else -1
     uint64_t cn, cd;             // Eq. 2 CPU term: link rate / Thpt_cpt as cn/cd (cn = 0: paper practice)
     uint64_t zn, zd;             // weight on Tiz (zn/zd = 1: the paper's Eq. 3)
+    // B200-calibrated Eq. 3 (cost_model = 1): each active list costs one random
+    // request (zr) plus its further lines at the stream rate (zs), in RTT units x zden.
+    // zr = 0: the paper's Eq. 3 with gamma.
+    uint64_t zr, zs, zden;
 };
 
 // Section 5.1 engine selection, evaluated identically on host (tests) and device.
 // t: partition edges, e: active edges, a: active vertices, z: zero-copy requests.
-__host__ __device__ inline int select_engine(uint64_t t, uint64_t e, uint64_t a, uint64_t z,
+__host__ __device__ inline int select_engine(uint64_t t, uint64_t e, uint64_t a, uint64_t z, uint64_t r,
                                              const CostParams &c) {
     if (e == 0) return ENG_NONE;
     typedef unsigned __int128 u128;
@@ -57,8 +61,14 @@ __host__ __device__ inline int select_engine(uint64_t t, uint64_t e, uint64_t a,
     }
     const uint64_t nz = (z + c.mr - 1) / c.mr;                            // Eq. 3 TLP count
     // Tiz = nz * RTT_zc, RTT_zc = gamma + (1-gamma) e/t  ->  nz*(gn t + (gd-gn) e) / (gd t)
-    const u128 num = (u128)nz * ((u128)c.gn * t + (u128)(c.gd - c.gn) * e) * c.zn;
-    const u128 den = (u128)c.gd * t * c.zd;
+    u128 num, den;
+    if (c.zr) {   // calibrated: (r*zr + (z - r)*zs) / zden
+        num = ((u128)r * c.zr + (u128)(z > r ? z - r : 0) * c.zs) * c.zn;
+        den = (u128)c.zden * c.zd;
+    } else {
+        num = (u128)nz * ((u128)c.gn * t + (u128)(c.gd - c.gn) * e) * c.zn;
+        den = (u128)c.gd * t * c.zd;
+    }
     const bool c1 = (u128)Tec * c.ad < (u128)c.an * Tef;                 // Tec < alpha Tef
     const bool c2 = (u128)Tec * c.bd * den < (u128)c.bn * num;            // Tec < beta Tiz
     if (c1 && c2) return ENG_C;
@@ -158,6 +168,9 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
 void launch_take_delta(const DevState &s, const QueueBufs &q, uint64_t e_lo, uint64_t e_hi, cudaStream_t st);
 void launch_range_queue(const DevState &s, uint64_t v_lo, uint64_t v_hi, RangeBufs r, cudaStream_t st);
 void launch_init_values(const DevState &s, uint64_t src_internal, const uint32_t *old_of, cudaStream_t st);
+// times a zero-copy probe over the mapped edge store (mode 0 random lines, 1 stream)
+float time_zc_probe(const uint4 *mapped, uint64_t nlines, int mode, uint32_t *sink, uint64_t *lines_read,
+                    cudaStream_t st);
 void launch_mark_improved(const uint32_t *val, const uint32_t *snap, uint64_t lo, uint64_t hi, uint32_t *bm,
                           cudaStream_t st);
 void launch_gather_out(const DevState &s, const uint32_t *new_id, void *out_dev, cudaStream_t st);

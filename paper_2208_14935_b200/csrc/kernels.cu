@@ -318,6 +318,55 @@ void launch_init_values(const DevState &s, uint64_t src_internal, const uint32_t
     k_init<<<(unsigned)blocks, 256, 0, st>>>(s, src_internal, old_of);
 }
 
+// Zero-copy probe for the calibrated cost model: random 128-byte lines (mode 0) or
+// a contiguous stream (mode 1) of the mapped edge store.
+__global__ void k_zc_probe(const uint4 *__restrict__ host, uint64_t nlines, uint64_t per_warp, int mode,
+                           uint32_t *__restrict__ sink) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    uint32_t acc = 0;
+    for (uint64_t i = 0; i < per_warp; i += 16) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint64_t line;
+            if (mode == 0) {
+                uint64_t x = (warp * 0x9E3779B97F4A7C15ull) ^ ((i + u * 4 + lane / 8) * 0xBF58476D1CE4E5B9ull);
+                x ^= x >> 31; x *= 0x94D049BB133111EBull; x ^= x >> 29;
+                line = x % nlines;
+            } else {
+                line = ((i + u * 4) * nwarps + warp) * 4 + lane / 8;
+                line %= nlines;
+            }
+            v[u] = host[line * 8 + (lane & 7)];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc ^= v[u].x;
+    }
+    if (acc == 0x9E3779B9u) *sink = acc;
+}
+
+float time_zc_probe(const uint4 *mapped, uint64_t nlines, int mode, uint32_t *sink, uint64_t *lines_read,
+                    cudaStream_t st) {
+    const int blocks = 148 * 2, threads = 256;
+    const uint64_t per_warp = 2048;    // 4 lines per warp instruction, 16 per step
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    k_zc_probe<<<blocks, threads, 0, st>>>(mapped, nlines, per_warp / 8, mode, sink);   // warm
+    cudaEventRecord(a, st);
+    k_zc_probe<<<blocks, threads, 0, st>>>(mapped, nlines, per_warp, mode, sink);
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *lines_read = (uint64_t)blocks * (threads / 32) * per_warp;
+    return ms;
+}
+
 // Multi-GPU: after the min-reduction, own vertices improved by another rank join
 // the next frontier (owner-side frontier merge).
 __global__ void k_mark_improved(const uint32_t *__restrict__ val, const uint32_t *__restrict__ snap, uint64_t lo,

@@ -129,13 +129,13 @@ __global__ void __launch_bounds__(kItemThreads) k_plan_items(PlanArgs A) {
     uint64_t ta = 0, te = 0, tz = 0;
     for (uint64_t pi = A.p_lo + threadIdx.x; pi < A.p_hi; pi += blockDim.x) {
         PartIter *P = &A.pb.parts[pi];
-        const uint64_t pe = __ldcg(&P->e), pa = __ldcg(&P->a), pz = __ldcg(&P->z);
+        const uint64_t pe = __ldcg(&P->e), pa = __ldcg(&P->a), pz = __ldcg(&P->z), pr = __ldcg(&P->ent);
         int p = ENG_NONE;
         if (pe > 0 && pi < A.cache_hi) {
             p = ENG_R;                   // edges resident in device memory: no transfer
         } else if (pe > 0) {
             switch (A.mode) {
-                case MODE_HYBRID: p = select_engine(A.t_static[pi], pe, pa, pz, A.cp); break;
+                case MODE_HYBRID: p = select_engine(A.t_static[pi], pe, pa, pz, pr, A.cp); break;
                 case MODE_FILTER: p = ENG_F; break;
                 case MODE_COMPACTION: p = ENG_C; break;
                 case MODE_ZEROCOPY: p = ENG_Z; break;

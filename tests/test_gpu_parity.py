@@ -350,3 +350,18 @@ def test_cpu_cost_term(hyt, algo):
     assert st["parts_compaction"] == 0
     if algo != "pr":
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+def test_calibrated_cost_model(hyt, algo):
+    """cost_model=1: costs measured on the box replace the PCIe-3
+    constants; only the engine choice changes, never the result."""
+    gkey = ("rmat", 5)
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    got, st, _ = run_gpu(hyt, g, algo, part=4096, cost_model=1)
+    want = expected(gkey, algo)
+    if algo == "pr":
+        assert_pr_close(got, want)
+    else:
+        assert np.array_equal(got, want)
+    assert st["cal_link_gbs"] > 1 and st["cal_zc_req_ns"] > 0 and st["cal_zc_line_ns"] > 0

@@ -52,6 +52,7 @@ def main():
                 try:
                     G.set("edge_cache", 1 if "+cache" in mode else 0)
                     G.set("cpu_cost", 1 if "+cpu" in mode else 0)
+                    G.set("cost_model", 1 if "+cal" in mode else 0)
                     zw = [x for x in mode.split("+") if x.startswith("zw")]
                     G.set("zc_weight", float(zw[0][2:]) if zw else 1.0)
                     G.set("engine_mode", mode.split("+")[0])
@@ -75,7 +76,9 @@ def main():
                                 "parts_f": st["parts_filter"], "parts_c": st["parts_compaction"],
                                 "parts_z": st["parts_zerocopy"], "parts_r": st["parts_resident"],
                                 "eng_ms": dict(zip(hyt.TAGS, st["eng_ms"])),
-                                "device_bytes_peak": st["device_bytes_peak"]})
+                                "device_bytes_peak": st["device_bytes_peak"],
+                                "calibration": [st["cal_link_gbs"], st["cal_cpt_gbs"], st["cal_zc_req_ns"],
+                                                st["cal_zc_line_ns"]]})
                 except hyt.HytError as ex:
                     row["error"] = str(ex)
                 print(json.dumps(row), flush=True)

@@ -46,6 +46,7 @@ def main():
     for mode in a.modes.split(","):
         G.set("edge_cache", 1 if "+cache" in mode else 0)
         G.set("cpu_cost", 1 if "+cpu" in mode else 0)
+        G.set("cost_model", 1 if "+cal" in mode else 0)
         zw = [x for x in mode.split("+") if x.startswith("zw")]
         G.set("zc_weight", float(zw[0][2:]) if zw else 1.0)
         G.set("engine_mode", mode.split("+")[0])
@@ -68,7 +69,8 @@ def main():
             row = {"mode": mode, "algo": algo, "ms": ms, "gteps": edges / (min(ms) / 1e3) / 1e9,
                    "iterations": st["iterations"], "transfer_over_edge_volume": link / (g.E * d1),
                    "parts": [st["parts_filter"], st["parts_compaction"], st["parts_zerocopy"], st["parts_resident"]],
-                   "device_bytes_peak": st["device_bytes_peak"]}
+                   "device_bytes_peak": st["device_bytes_peak"],
+                   "calibration": [st["cal_link_gbs"], st["cal_cpt_gbs"], st["cal_zc_req_ns"], st["cal_zc_line_ns"]]}
             if a.check:
                 t = time.time()
                 if algo == "bfs":
