@@ -299,6 +299,9 @@ def main():
         else:
             edges_per[a] = g.E
 
+    st0 = G.stats()
+    calib = {"link_gbs": st0["cal_link_gbs"], "thpt_cpt_gbs": st0["cal_cpt_gbs"],
+             "zc_request_ns": st0["cal_zc_req_ns"], "zc_line_ns": st0["cal_zc_line_ns"]}
     # ---- timed region ----
     cur = torch.cuda.current_stream()
     times, per_algo_ms, launches = [], {a: [] for a in algos}, 0
@@ -431,6 +434,8 @@ def main():
         "config": {"workload": workload_desc(args.config, args.shift, algos),
                    "budget_gb": args.budget_gb, "engine_mode": args.engine, "partition_bytes": 32 << 20,
                    "params": args.set,
+                   "cost_model": "calibrated on this box (SURVEY §8f #2; cost_model=0 is the paper's PCIe-3 rule)",
+                   "calibration": calib,
                    "parallelism": f"vertex-range x{world}" if world > 1 else "single GPU",
                    "l2": L2_NOTE, "degree_stats": dstats},
         "per_algo": per_algo,

@@ -167,10 +167,12 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   link rate and Thpt_cpt calibrated on this box (or set by link_gbs /
  *   thpt_cpt_gbs); the paper omits the term in selection, so 0 is the
  *   paper's rule; zc_weight [1.0] multiplies Tiz (Eq. 3)
- *   before the comparisons (1 = the paper); cost_model [0]: 1 replaces the
+ *   before the comparisons (1 = the paper); cost_model [1]: 1 replaces the
  *   PCIe-3 constants by costs measured on this box -- Eq. 2's CPU term as with
  *   cpu_cost, and Eq. 3 as (active lists x random-request time + further lines
- *   x streamed-line time) / RTT, both probed on the mapped edge store.
+ *   x streamed-line time) / RTT, probed once per process on a pinned buffer
+ *   (zc_req_ns / zc_line_ns / link_gbs / thpt_cpt_gbs override the probes);
+ *   0 is the paper's rule with its PCIe-3 constants.
  * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
 int hyt_set_param(hyt_graph *g, const char *key, double value);
 

@@ -90,7 +90,9 @@ def _L():
         L.oracle_tec.restype = u64
         L.oracle_select.argtypes = [u64, u64, u64, u64, cp]
         L.oracle_select.restype = i32
-        L.oracle_plan.argtypes = [u64, vp, vp, vp, u64, vp, cp] + [vp] * 7
+        L.oracle_plan.argtypes = [u64, vp, vp, vp, u64, vp, cp, vp] + [vp] * 7
+        L.oracle_select_cal.argtypes = [u64, u64, u64, u64, u64, cp, vp]
+        L.oracle_select_cal.restype = i32
         L.oracle_plan.restype = ctypes.c_int64
         L.oracle_combine.argtypes = [u64, vp, u64, vp]
         L.oracle_combine.restype = ctypes.c_int64
@@ -236,6 +238,28 @@ def select(t: int, e: int, a: int, z: int, cfg: CostCfg) -> int:
     return _L().oracle_select(t, e, a, z, ctypes.byref(c))
 
 
+class _Cal(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("cpu_num", "cpu_den", "zr_num", "zs_num", "z_den")]
+
+
+@dataclass
+class Cal:
+    """Calibrated constants as exact rationals: link/Thpt_cpt, and the zero-copy
+    random-request (zr) and streamed-line (zs) costs in RTT units."""
+    cpu: Fraction
+    zr: Fraction
+    zs: Fraction
+
+    def c(self) -> _Cal:
+        den = self.zr.denominator * self.zs.denominator
+        return _Cal(self.cpu.numerator, self.cpu.denominator, int(self.zr * den), int(self.zs * den), den)
+
+
+def select_cal(t: int, e: int, a: int, z: int, r: int, cfg: CostCfg, cal: Cal) -> int:
+    c, k = cfg.c(), cal.c()
+    return _L().oracle_select_cal(t, e, a, z, r, ctypes.byref(c), ctypes.byref(k))
+
+
 @dataclass
 class Plan:
     t: np.ndarray
@@ -247,7 +271,7 @@ class Plan:
     units: list
 
 
-def plan(off, active, bounds, cfg: CostCfg, din=None) -> Plan:
+def plan(off, active, bounds, cfg: CostCfg, din=None, cal: Cal = None) -> Plan:
     off = np.ascontiguousarray(off, dtype=np.uint64)
     V = len(off) - 1
     active = np.ascontiguousarray(active, dtype=np.uint8)
@@ -259,7 +283,9 @@ def plan(off, active, bounds, cfg: CostCfg, din=None) -> Plan:
     if din is not None:
         din = np.ascontiguousarray(din, dtype=np.uint64)
     c = cfg.c()
+    k = cal.c() if cal is not None else None
     nu = _L().oracle_plan(V, _p(off), _p(din), _p(active), N, _p(bounds), ctypes.byref(c),
+                          ctypes.byref(k) if k is not None else None,
                           _p(t), _p(e), _p(a), _p(z), _p(hub), _p(p), _p(units))
     return Plan(t, e, a, z, hub, p, [(int(units[2 * j]), int(units[2 * j + 1])) for j in range(nu)])
 

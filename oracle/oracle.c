@@ -457,6 +457,37 @@ int64_t oracle_combine(uint64_t N, const uint8_t *p, uint64_t k, uint64_t *units
 }
 
 /* ===================================================================== */
+/* The B200-calibrated variant of the section 5.1 rule (DESIGN.md          */
+/* "Calibrated cost model").  All costs are in RTT units,    */
+/* RTT = the time of one saturated TLP (m*MR bytes) at the DMA link rate:  */
+/*   Tef = ceil(t*d1/(m*MR))                              (Eq. 1)          */
+/*   Tec = ceil(B/(m*MR)) + ceil(B * link/Thpt_cpt / (m*MR)),              */
+/*         B = e*d1 + a*d2        (Eq. 2 with its CPU term)      */
+/*   Tiz = r*zr + (z - r)*zs      (Eq. 3 re-fit: each of the r active lists */
+/*         costs one random request zr, each further line a streamed zs)   */
+/* with link/Thpt_cpt = cpu_num/cpu_den, zr = zr_num/z_den, zs = zs_num/z_den. */
+/* The decision rule itself is unchanged (ties -> F).           */
+/* ===================================================================== */
+typedef struct { uint64_t cpu_num, cpu_den, zr_num, zs_num, z_den; } oracle_cal;
+
+int oracle_select_cal(uint64_t t, uint64_t e, uint64_t a, uint64_t z, uint64_t r, const oracle_cost_cfg *c,
+                      const oracle_cal *k) {
+    if (e == 0) return 0;
+    typedef unsigned __int128 u128;
+    const uint64_t tlp = c->m * c->mr;
+    const uint64_t B = e * c->d1 + a * c->d2;
+    const uint64_t Tef = ceil_div(t * c->d1, tlp);
+    const u128 cpu_n = (u128)B * k->cpu_num, cpu_d = (u128)k->cpu_den * tlp;
+    const uint64_t Tec = ceil_div(B, tlp) + (uint64_t)((cpu_n + cpu_d - 1) / cpu_d);
+    const u128 tiz_num = (u128)r * k->zr_num + (u128)(z - r) * k->zs_num;   /* / z_den */
+    const int c1 = (u128)Tec * c->alpha_den < (u128)c->alpha_num * Tef;
+    const int c2 = (u128)Tec * c->beta_den * k->z_den < (u128)c->beta_num * tiz_num;
+    if (c1 && c2) return 2;
+    if (tiz_num < (u128)Tef * k->z_den) return 3;
+    return 1;
+}
+
+/* ===================================================================== */
 /* Algorithm 1 on a frontier snapshot, step by step.           */
 /* Inputs: V, off (the graph the engines see), active[V] (0/1), bounds.    */
 /* Per partition i: t_i, e_i, a_i, z_i, hub score (sum D_o*D_i over        */
@@ -466,23 +497,24 @@ int64_t oracle_combine(uint64_t N, const uint8_t *p, uint64_t k, uint64_t *units
 /* Returns the number of F units.                                          */
 /* ===================================================================== */
 int64_t oracle_plan(uint64_t V, const uint64_t *off, const uint64_t *din, const uint8_t *active,
-                    uint64_t N, const uint64_t *bounds, const oracle_cost_cfg *c,
+                    uint64_t N, const uint64_t *bounds, const oracle_cost_cfg *c, const oracle_cal *cal,
                     uint64_t *t_out, uint64_t *e_out, uint64_t *a_out, uint64_t *z_out,
                     uint64_t *hub_out, uint8_t *p_out, uint64_t *units) {
     (void)V;
     for (uint64_t i = 0; i < N; ++i) {
-        uint64_t t = 0, e = 0, a = 0, z = 0, hub = 0;
+        uint64_t t = 0, e = 0, a = 0, z = 0, hub = 0, r = 0;
         for (uint64_t v = bounds[i]; v < bounds[i + 1]; ++v) {
             uint64_t deg = off[v + 1] - off[v];
             t += deg;
             if (!active[v]) continue;
             a += 1;
             e += deg;
+            r += deg > 0;
             z += oracle_zc_requests(off[v], deg, c);
             if (din) hub += deg * din[v];
         }
         t_out[i] = t; e_out[i] = e; a_out[i] = a; z_out[i] = z; hub_out[i] = hub;
-        p_out[i] = (uint8_t)oracle_select(t, e, a, z, c);
+        p_out[i] = (uint8_t)(cal ? oracle_select_cal(t, e, a, z, r, c, cal) : oracle_select(t, e, a, z, c));
     }
     return oracle_combine(N, p_out, c->k, units);
 }

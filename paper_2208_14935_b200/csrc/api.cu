@@ -111,6 +111,8 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "cpu_cost") { integral(); in(0, 1); p.cpu_cost = (int)v; }
         else if (k == "zc_weight") { in(0.001, 1000); p.zc_weight = v; }
         else if (k == "cost_model") { integral(); in(0, 1); p.cost_model = (int)v; }
+        else if (k == "zc_req_ns") { in(0, 1e6); p.zc_req_ns = v; g->est_zc_req_ns = v; }
+        else if (k == "zc_line_ns") { in(0, 1e6); p.zc_line_ns = v; g->est_zc_line_ns = v; }
         else if (k == "thpt_cpt_gbs") { in(0, 1e6); p.thpt_cpt_gbs = v; g->est_cpt_gbs = v; }
         else if (k == "link_gbs") { in(0, 1e6); p.link_gbs = v; g->est_link_gbs = v; }
         else throw Err{HYT_EINVAL, "unknown parameter '" + k + "'"};

@@ -74,7 +74,9 @@ struct Params {
     double thpt_cpt_gbs = 0;   // host gather throughput (0 = measure)
     double link_gbs = 0;       // host->device link rate (0 = measure)
     double zc_weight = 1.0;    // multiplier on Tiz (1 = the paper's Eq. 3)
-    int cost_model = 0;        // 0: the paper's Eq. 1-3 (PCIe-3 constants); 1: calibrated on this box
+    int cost_model = 1;        // 1: Eq. 1-3 with costs calibrated on this box; 0: the paper's PCIe-3 constants
+    double zc_req_ns = 0;      // zero-copy random 128-B request time (0 = measure)
+    double zc_line_ns = 0;     // zero-copy streamed 128-B line time (0 = measure)
 };
 
 CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio = 0.0, double zr_rtt = 0.0,

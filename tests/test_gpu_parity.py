@@ -197,10 +197,17 @@ def test_hub_sort_permutation_matches_oracle(hyt):
             G.close()
 
 
+@pytest.mark.parametrize("cost_model", [0, 1])
 @pytest.mark.parametrize("algo,d1", [("bfs", 4), ("sssp", 8)])
-def test_plan_parity(hyt, algo, d1):
+def test_plan_parity(hyt, algo, d1, cost_model):
     """the GPU's per-partition aggregates and engine choices equal the
-    oracle's Algorithm 1 on the same frontier snapshot, bit-exact."""
+    oracle's Algorithm 1 on the same frontier snapshot, bit-exact: with the paper's
+    PCIe-3 constants (cost_model=0) and with the calibrated rule (cost_model=1) under
+    fixed constants (link 50 GB/s, Thpt_cpt 10 GB/s, 13.1072 ns per random zero-copy
+    request, 2.62144 ns per streamed line: link/Thpt_cpt = 5, zr = 1/50 RTT,
+    zs = 1/250 RTT with RTT = 32768 B / 50 GB/s)."""
+    from fractions import Fraction
+    cal = oracle.Cal(Fraction(5), Fraction(1, 50), Fraction(1, 250)) if cost_model else None
     for gkey in [("rmat", 3), ("rmat", 8), ("rmat", 12)]:
         g = gkey_graph(gkey)
         new_id = oracle.hub_sort(g.off, g.nbr)
@@ -209,6 +216,10 @@ def test_plan_parity(hyt, algo, d1):
         G = hyt.Graph(device=0)
         try:
             G.load(g.off, g.nbr, g.w)
+            G.set("cost_model", cost_model)
+            if cost_model:
+                for k, v in (("link_gbs", 50), ("thpt_cpt_gbs", 10), ("zc_req_ns", 13.1072), ("zc_line_ns", 2.62144)):
+                    G.set(k, v)
             for part in (4096, 65536):
                 G.set("partition_bytes", part)
                 for dens in (0.001, 0.02, 0.3, 1.0):
@@ -218,7 +229,7 @@ def test_plan_parity(hyt, algo, d1):
                     act2[new_id] = act
                     bounds = oracle.partition(off2, d1, part)
                     assert np.array_equal(gp["bounds"], bounds)
-                    op = oracle.plan(off2, act2, bounds, oracle.CostCfg(d1=d1))
+                    op = oracle.plan(off2, act2, bounds, oracle.CostCfg(d1=d1), cal=cal)
                     for f in ("t", "e", "a", "z", "p"):
                         assert np.array_equal(gp[f], getattr(op, f).astype(gp[f].dtype)), (gkey, part, dens, f)
         finally:

@@ -251,3 +251,64 @@ def test_plan_aggregates_plain_definition(seed):
                 assert pl.z[i] == req[sl][act].sum()
                 assert pl.p[i] == oracle.select(int(pl.t[i]), int(pl.e[i]), int(pl.a[i]), int(pl.z[i]), cfg)
             assert pl.units == oracle.combine(pl.p, 4)
+
+
+# ------------------------------------------------------------- calibrated rule (§8f #2)
+
+def calibrated_rule(t, e, a, z, r, d1, cpu, zr, zs, d2=4, m=128, MR=256):
+    """DESIGN.md 'Calibrated cost model' restated with Fractions: Eq. 1, Eq. 2 with its
+    CPU term, Eq. 3 as r random requests + (z - r) streamed lines, and the
+    unchanged §5.1 decision rule."""
+    alpha, beta = Fraction("0.8"), Fraction("0.4")
+    if e == 0:
+        return oracle.NONE
+    tlp = m * MR
+    B = e * d1 + a * d2
+    Tef = ceil(Fraction(t * d1, tlp))
+    Tec = ceil(Fraction(B, tlp)) + ceil(Fraction(B, tlp) * cpu)
+    Tiz = r * zr + (z - r) * zs
+    if Tec < alpha * Tef and Tec < beta * Tiz:
+        return oracle.C
+    if Tiz < Tef:
+        return oracle.Z
+    return oracle.F
+
+
+CAL = oracle.Cal(Fraction(5), Fraction(1, 50), Fraction(1, 250))   # DESIGN.md test constants
+
+
+@pytest.mark.parametrize("d1", [4, 8])
+def test_calibrated_select_matches_restatement(d1):
+    rng = random.Random(100 + d1)
+    cfg = oracle.CostCfg(d1=d1)
+    counts = {0: 0, 1: 0, 2: 0, 3: 0}
+    for _ in range(10000):
+        t, e, a, z = random_case(rng, d1)
+        r = 0 if a == 0 else rng.randint(max(1, a // 2), a)        # lists with >= 1 edge
+        z = max(z, r)
+        want = calibrated_rule(t, e, a, z, r, d1, CAL.cpu, CAL.zr, CAL.zs)
+        assert oracle.select_cal(t, e, a, z, r, cfg, CAL) == want, (t, e, a, z, r)
+        counts[want] += 1
+    assert min(counts[1], counts[2], counts[3]) > 100          # every engine exercised
+
+
+def test_calibrated_worked_examples():
+    cfg = oracle.CostCfg(d1=4)
+    # S:273 analog: one active degree-32 vertex in a 1M-edge partition -> Z
+    # (Tef = 123, Tec = 1 + ceil(132*5/32768) = 2, Tiz = 1/50)
+    assert oracle.select_cal(1_000_000, 32, 1, 1, 1, cfg, CAL) == oracle.Z
+    # a saturated partition (every line requested) -> F: Tiz = 256/50 > Tef = 1
+    assert oracle.select_cal(8192, 8192, 256, 256, 256, cfg, CAL) == oracle.F
+    # a slow host gather removes compaction: huge cpu ratio
+    slow = oracle.Cal(Fraction(10**6), CAL.zr, CAL.zs)
+    assert oracle.select_cal(1_000_000, 50_000, 20_000, 20_000, 20_000, cfg, slow) != oracle.C
+
+
+def test_calibrated_fig5():
+    # Fig. 5 (P:286): same active-edge ratio, the 6-list subset costs twice the 3-list one
+    t = gold("fig5_toy.json")
+    cfg = oracle.CostCfg(d1=t["d1"])
+    g6 = sum(zr for zr in [CAL.zr] * 6)
+    g3 = sum(zr for zr in [CAL.zr] * 3)
+    assert g6 == 2 * g3
+    assert oracle.select_cal(128, 64, 6, 6, 6, cfg, CAL) == oracle.select_cal(128, 64, 3, 3, 3, cfg, CAL) == oracle.Z
