@@ -95,8 +95,8 @@ __device__ __forceinline__ void red_add_keep(float *p, float x, uint64_t pol) {
     asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(x), "l"(pol) : "memory");
 }
 
-template <int ALGO, bool COMPACT>
-__global__ void __launch_bounds__(kRelaxThreads, 4)
+template <int ALGO, bool COMPACT, int MINB>
+__global__ void __launch_bounds__(kRelaxThreads, MINB)
 k_relax(RelaxArgs A) {
     constexpr uint32_t D1 = (ALGO == ALGO_SSSP) ? 8u : 4u;
     constexpr int EPC = 16 / D1;                  // edge records per chunk
@@ -262,7 +262,7 @@ k_relax(RelaxArgs A) {
 
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
-                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st) {
+                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb) {
     RelaxArgs A;
     A.s = s; A.qv = q.qv; A.qpre = q.qpre; A.qbeg = q.qbeg; A.qdeg = q.qdeg; A.qaux = q.qaux;
     A.tile = q.tile + tile_base;
@@ -277,15 +277,18 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
         if (grid > (uint64_t)max_ctas) grid = (uint64_t)max_ctas;
     }
     if (grid == 0) grid = 1;
-#define HYT_RELAX(ALG)                                                                       \
-    if (src.compact) k_relax<ALG, true><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);      \
-    else k_relax<ALG, false><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);
+#define HYT_RELAX_B(ALG, MB)                                                                     \
+    if (src.compact) k_relax<ALG, true, MB><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);      \
+    else k_relax<ALG, false, MB><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);
+#define HYT_RELAX(ALG)                                                                           \
+    if (minb >= 6) { HYT_RELAX_B(ALG, 6) } else if (minb == 5) { HYT_RELAX_B(ALG, 5) } else { HYT_RELAX_B(ALG, 4) }
     switch (s.algo) {
         case ALGO_BFS: HYT_RELAX(ALGO_BFS); break;
         case ALGO_SSSP: HYT_RELAX(ALGO_SSSP); break;
         case ALGO_CC: HYT_RELAX(ALGO_CC); break;
         default: HYT_RELAX(ALGO_PR); break;
     }
+#undef HYT_RELAX_B
 #undef HYT_RELAX
 }
 
