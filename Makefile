@@ -24,7 +24,7 @@ hytgen/libhytgen.so: hytgen/hytgen.c
 oracle/liboracle.so: oracle/oracle.c
 	gcc -O2 -fPIC -shared -o $@ $< -lm
 
-tools: tools/pin_bench tools/zc_bench
+tools: tools/pin_bench tools/zc_bench tools/scatter_bench
 
 tools/pin_bench: tools/pin_bench.cu
 	$(NVCC) $(ARCH) -O2 -o $@ $< -lpthread
@@ -32,7 +32,10 @@ tools/pin_bench: tools/pin_bench.cu
 tools/zc_bench: tools/zc_bench.cu
 	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
 
+tools/scatter_bench: tools/scatter_bench.cu
+	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
+
 clean:
-	rm -rf build $(LIB) hytgen/libhytgen.so oracle/liboracle.so
+	rm -rf build $(LIB) hytgen/libhytgen.so oracle/liboracle.so tools/pin_bench tools/zc_bench tools/scatter_bench
 
 .PHONY: all clean tools

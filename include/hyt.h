@@ -173,6 +173,10 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   x streamed-line time) / RTT, probed once per process on a pinned buffer
  *   (zc_req_ns / zc_line_ns / link_gbs / thpt_cpt_gbs override the probes);
  *   0 is the paper's rule with its PCIe-3 constants.
+ *   Kernel tuning (no effect on results): relax_ctas_per_sm [4],
+ *   zc_ctas_per_sm [2], relax_minb [4] (__launch_bounds__ min CTAs/SM, 4..6),
+ *   relax_hot [1] (hub block ids < 4096 in shared memory: PR delta
+ *   accumulation, min-algorithm value copy; 0 off, 1 auto, 2 always).
  * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
 int hyt_set_param(hyt_graph *g, const char *key, double value);
 

@@ -68,6 +68,7 @@ struct Params {
     uint64_t compaction_buffer_bytes = 0;
     int zc_ctas_per_sm = 2;
     int relax_ctas_per_sm = 4;
+    int relax_hot = 1;         // hub block in smem (PR Δ accumulation / min-algorithm value copy): 0 off, 1 auto, 2 always
     int relax_minb = 4;        // __launch_bounds__ min CTAs/SM of the relax kernel (4: 64 regs, 5: 51, 6: 42)
     int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
     uint64_t edge_cache_bytes = 0;   // cap on the cache (0 = whatever the budget leaves)

@@ -164,7 +164,7 @@ struct EdgeSrc {
 // with seg_chunks chunks; dev_tot (range queues) overrides seg_end/seg_chunks/c_hi.
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
-                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb = 4);
+                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb = 4, int hot = 1);
 void launch_take_delta(const DevState &s, const QueueBufs &q, uint64_t e_lo, uint64_t e_hi, cudaStream_t st);
 void launch_range_queue(const DevState &s, uint64_t v_lo, uint64_t v_hi, RangeBufs r, cudaStream_t st);
 void launch_init_values(const DevState &s, uint64_t src_internal, const uint32_t *old_of, cudaStream_t st);

@@ -43,9 +43,13 @@ void launch_pr_frontier(const DevState &s, cudaStream_t st) {
 // the entry of each of its 4 chunks from a 128-bit map of entry start positions
 // (one popc) and issues 4 independent
 // 16-byte loads; 8 consecutive lanes cover one aligned 128-byte line.
-// PR: pushes into the hub block (ids < kHotV, the highest-H vertices after hub
-// sorting) are accumulated in shared memory and flushed once per CTA, so
-// the hottest destinations do not serialise L2 atomics.
+// Hub block (ids < kHotV, the highest-H vertices after hub sorting):
+// PR pushes into it are accumulated in shared memory and flushed once per CTA, so
+// the hottest destinations do not serialise L2 atomics.  Min-algorithms keep a
+// per-CTA copy of the hub values: values only decrease, so the copy is never below
+// the global value and a candidate that does not beat it cannot beat the global
+// one either.  A candidate that lowers the copy (smem atomicMin) goes on to the
+// global atomicMin, so at most a few global atomics per hub per CTA remain.
 // ---------------------------------------------------------------------------
 struct RelaxArgs {
     DevState s;
@@ -60,6 +64,7 @@ struct RelaxArgs {
     const uint64_t *dev_tot;   // optional: [0] = entry count, [1] = chunk total (range queues)
     const uint4 *base;
     int64_t shift;
+    uint32_t n_hot;            // hub-block size cached in shared memory (0 = off)
 };
 
 constexpr int kWarps = kRelaxThreads / 32;
@@ -106,7 +111,8 @@ k_relax(RelaxArgs A) {
     __shared__ uint32_t s_deg[kWarps][kTile + 1];
     __shared__ uint32_t s_src[kWarps][kTile + 1];
     __shared__ uint32_t s_mask[kWarps][kChunksPerThread];
-    __shared__ float s_hot[PR ? kHotV : 1];
+    __shared__ uint32_t s_hotw[kHotV];            // PR: f32 Δ accumulators; else hub values
+    float *s_hot = reinterpret_cast<float *>(s_hotw);
     const DevState &S = A.s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
@@ -117,9 +123,10 @@ k_relax(RelaxArgs A) {
         seg_chunks = A.dev_tot[1];
         c_hi = seg_chunks;
     }
-    const uint32_t n_hot = PR ? (uint32_t)min((uint64_t)kHotV, S.V) : 0u;
-    if constexpr (PR) {
-        for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x) s_hot[i] = 0.0f;
+    const uint32_t n_hot = A.n_hot;
+    if (n_hot) {
+        for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x)
+            s_hotw[i] = PR ? 0u : ld_keep(&S.val[i], pol_keep);
         __syncthreads();
     }
     if (c_hi > c_lo) {
@@ -224,7 +231,7 @@ k_relax(RelaxArgs A) {
                             } else cnd = src;
                             dst[rr][qd] = d;
                             cand[rr][qd] = ok ? cnd : kInf;
-                            cur[rr][qd] = ok ? ld_keep(&S.val[d], pol_keep) : 0u;
+                            cur[rr][qd] = !ok ? 0u : d < n_hot ? s_hotw[d] : ld_keep(&S.val[d], pol_keep);
                         }
                     }
                     // issue every improving atomicMin first (their round trips overlap),
@@ -237,7 +244,11 @@ k_relax(RelaxArgs A) {
 #pragma unroll
                         for (int qd = 0; qd < EPC; ++qd) {
                             old[rr][qd] = 0u;          // "not issued": never marks
-                            if (cand[rr][qd] < cur[rr][qd]) old[rr][qd] = atomicMin(&S.val[dst[rr][qd]], cand[rr][qd]);
+                            const uint32_t d = dst[rr][qd], cn = cand[rr][qd];
+                            if (cn < cur[rr][qd]) {
+                                if (d < n_hot && cn >= atomicMin(&s_hotw[d], cn)) continue;
+                                old[rr][qd] = atomicMin(&S.val[d], cn);
+                            }
                         }
 #pragma unroll
                     for (int rr = 0; rr < 2; ++rr)
@@ -251,7 +262,7 @@ k_relax(RelaxArgs A) {
             __syncwarp();
         }
     }
-    if constexpr (PR) {
+    if (PR && n_hot) {
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x) {
             const float x = s_hot[i];
@@ -262,7 +273,7 @@ k_relax(RelaxArgs A) {
 
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
-                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb) {
+                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb, int hot) {
     RelaxArgs A;
     A.s = s; A.qv = q.qv; A.qpre = q.qpre; A.qbeg = q.qbeg; A.qdeg = q.qdeg; A.qaux = q.qaux;
     A.tile = q.tile + tile_base;
@@ -277,6 +288,14 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
         if (grid > (uint64_t)max_ctas) grid = (uint64_t)max_ctas;
     }
     if (grid == 0) grid = 1;
+    // PR: always (the flush touches only non-zero accumulators).  Min-algorithms:
+    // only when every warp has >= 4 tiles (64 KiB of edges per CTA against the 16 KiB
+    // hub-value load); range queues (device-side size) do not qualify.  hot = 2
+    // forces it on (tests), 0 turns both off.
+    const uint64_t hv = s.V < (uint64_t)kHotV ? s.V : (uint64_t)kHotV;
+    A.n_hot = 0;
+    if (hot && s.algo == ALGO_PR) A.n_hot = (uint32_t)hv;
+    else if (hot == 2 || (hot == 1 && !dev_tot && (c_hi - c_lo) >= grid * kWarps * 4 * kTile)) A.n_hot = (uint32_t)hv;
 #define HYT_RELAX_B(ALG, MB)                                                                     \
     if (src.compact) k_relax<ALG, true, MB><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);      \
     else k_relax<ALG, false, MB><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);

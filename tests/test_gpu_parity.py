@@ -376,3 +376,20 @@ def test_calibrated_cost_model(hyt, algo):
     else:
         assert np.array_equal(got, want)
     assert st["cal_link_gbs"] > 1 and st["cal_zc_req_ns"] > 0 and st["cal_zc_line_ns"] > 0
+
+
+@pytest.mark.parametrize("hot", [0, 2])
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+@pytest.mark.parametrize("gkey", [("rmat", 9), ("rmat", 13), ("crafted", 2)], ids=lambda k: f"{k[0]}{k[1]}")
+def test_relax_hub_block(hyt, hot, engine, algo, gkey):
+    """relax_hot: the hub block (ids < 4096) in shared memory -- PR Δ accumulators,
+    min-algorithm per-CTA value copies -- forced on for every launch (2) or off (0);
+    results identical to the oracle either way (a kernel tuning knob only)."""
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    got, st, log = run_gpu(hyt, g, algo, engine=engine, part=4096, relax_hot=hot)
+    want = expected(gkey, algo)
+    if algo == "pr":
+        assert_pr_close(got, want)
+    else:
+        assert np.array_equal(got, want)

@@ -69,9 +69,31 @@ def main():
                 json.dump(last_json(src), f, indent=1)
     if os.path.exists(os.path.join(G, "bench_detail.json")):
         exec_path(os.path.join(G, "bench_detail.json"), os.path.join(P, f"{r}_exec_path_tw.md"))
-    if os.path.exists(os.path.join(G, "modes.json")):
-        modes(os.path.join(G, "modes.json"), os.path.join(P, f"{r}_modes_tw.md"))
-    for csvname, tag in (("launches_full.csv", "launches_bench"),):
+    for src, dst in (("modes_final.json", "modes_tw"), ("modes.json", "modes_tw")):
+        if os.path.exists(os.path.join(G, src)):
+            modes(os.path.join(G, src), os.path.join(P, f"{r}_{dst}.md"))
+            break
+    cfg_lines = ["# Full-size configurations (tools/run_configs.py, warm runs, O(E) certificates where run)\n",
+                 "| config | V | E | budget GB | algo | mode | ms (runs) | iterations | transfer/edge | F/C/Z/R partitions | certificate |",
+                 "|---|---:|---:|---:|---|---|---|---:|---:|---|---|"]
+    for name in ("cfg_fr.json", "cfg_fr_cal.json", "cfg_uk.json", "cfg_uk_cal.json"):
+        path = os.path.join(G, name)
+        if not os.path.exists(path):
+            continue
+        d = json.load(open(path))
+        for row in d["rows"]:
+            cert = row.get("certificate", "")
+            if isinstance(cert, dict):
+                cert = f"res_l1 {cert['res_l1']:.1f}, max rel res {cert['max_rel_res']:.1e}"
+            cfg_lines.append(f"| {d['config']} | {d['V']} | {d['E']} | {d['budget_gb']} | {row['algo']} | {row['mode']} | "
+                             f"{', '.join(f'{x:.1f}' for x in row['ms'])} | {row['iterations']} | "
+                             f"{row['transfer_over_edge_volume']:.2f} | {'/'.join(str(x) for x in row['parts'])} | {cert} |")
+    open(os.path.join(P, f"{r}_configs_full_size.md"), "w").write("\n".join(cfg_lines) + "\n")
+    for src in ("zc_bench.json", "scatter_bench.json", "sweep_hot.json"):
+        if os.path.exists(os.path.join(G, src)):
+            import shutil
+            shutil.copy(os.path.join(G, src), os.path.join(P, f"{r}_{src}"))
+    for csvname, tag in (("launches_w1.csv", "launches_bench"),):
         src = os.path.join(G, csvname)
         if os.path.exists(src):
             out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), "launches", src],
