@@ -239,6 +239,14 @@ int hyt_select_engine(const hyt_graph *g, uint64_t t, uint64_t e, uint64_t a, ui
 int hyt_nccl_unique_id(void *uid_out_128_bytes);
 int hyt_init_dist(hyt_graph *g, int rank, int world, const void *nccl_uid_128_bytes);
 
+/* The same multi-rank protocol with an in-process transport: `world` handles in
+ * one process, each driven by its own thread (they may share one GPU), join
+ * group `group` (any key the threads agree on).  The reductions go through host
+ * memory in rank order.  For testing the multi-rank path on one device; a job
+ * uses hyt_init_dist.  Call before hyt_load_csr.  A rank waiting more than
+ * 300 s for the others fails with HYT_ENCCL.  Errors: HYT_EINVAL, HYT_ESTATE. */
+int hyt_init_dist_local(hyt_graph *g, int rank, int world, uint64_t group);
+
 /* The vertex-range split of a multi-GPU job (host routine the library uses,
  * exposed for CPU tests): with the greedy partitions of `partition_bytes` at
  * record width d1 over off_host (u64[V+1], the graph as loaded), rank `rank` of

@@ -75,6 +75,7 @@ _SIGS = {
     "hyt_nccl_unique_id": ([_vp], _i32),
     "hyt_rank_range": ([_vp, _u64, _u64, _u64, _i32, _i32] + [ctypes.POINTER(_u64)] * 4, ctypes.c_int64),
     "hyt_init_dist": ([_vp, _i32, _i32, _vp], _i32),
+    "hyt_init_dist_local": ([_vp, _i32, _i32, _u64], _i32),
     "hyt_free": ([_vp], None),
     "hyt_last_error": ([], ctypes.c_char_p),
     "hyt_version": ([], ctypes.c_char_p),
@@ -144,6 +145,10 @@ class Graph:
     def init_dist(self, rank: int, world: int, uid: bytes) -> None:
         buf = ctypes.create_string_buffer(bytes(uid), 128)
         check(hyt_init_dist(self.h, rank, world, buf), "hyt_init_dist")
+
+    def init_dist_local(self, rank: int, world: int, group: int) -> None:
+        """Join an in-process group (one thread per rank; testing the multi-rank path on one GPU)."""
+        check(hyt_init_dist_local(self.h, rank, world, group), "hyt_init_dist_local")
 
     def load(self, off, nbr, w=None, hubsort: bool = True) -> None:
         off = np.ascontiguousarray(off, dtype=np.uint64)

@@ -212,6 +212,16 @@ int hyt_init_dist(hyt_graph *g, int rank, int world, const void *uid) {
     })
 }
 
+int hyt_init_dist_local(hyt_graph *g, int rank, int world, uint64_t group) {
+    HYT_GUARD({
+        HYT_REQUIRE(g, HYT_EINVAL, "null argument");
+        HYT_REQUIRE(world >= 1 && rank >= 0 && rank < world, HYT_EINVAL, "bad rank/world");
+        HYT_REQUIRE(!g->loaded, HYT_ESTATE, "call hyt_init_dist_local before hyt_load_csr");
+        HYT_REQUIRE(!g->nccl_comm && !g->local_group, HYT_ESTATE, "handle already joined a group");
+        dist_init_local(g, rank, world, group);
+    })
+}
+
 void hyt_free(hyt_graph *g) {
     if (!g) return;
     try { free_graph(g); } catch (...) {}

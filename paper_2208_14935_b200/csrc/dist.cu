@@ -3,8 +3,19 @@
 // (min for BFS/SSSP/CC, sum for PR deltas).  NCCL is resolved at run time with
 // dlopen (the torch-bundled libnccl.so.2 when torch is loaded), so the library
 // has no link-time NCCL dependency.
+//
+// A second transport, the in-process group (hyt_init_dist_local), runs the same
+// reductions through host memory between threads of one process, each thread
+// owning one handle (all on one GPU if need be).  It exists so the multi-rank
+// path -- split, exchange, frontier merge, termination -- executes on the one GPU
+// a test box has; a job uses NCCL.
 #include <dlfcn.h>
+#include <chrono>
+#include <condition_variable>
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include "graph.h"
 
 namespace hyt {
@@ -55,6 +66,85 @@ static NcclApi &nccl() {
                                      (nccl().GetErrorString ? nccl().GetErrorString(_r) : "?")}; \
     } while (0)
 
+// ---------------------------------------------------------------------------
+// in-process group
+// ---------------------------------------------------------------------------
+struct LocalGroup {
+    int world = 0, members = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    uint64_t gen = 0;
+    int arrived = 0;
+    std::vector<std::vector<uint8_t>> slot;
+    std::vector<uint8_t> result;
+};
+static std::mutex g_groups_mu;
+static std::map<uint64_t, std::shared_ptr<LocalGroup>> g_groups;
+
+static void local_barrier(LocalGroup &G) {
+    std::unique_lock<std::mutex> l(G.mu);
+    const uint64_t my = G.gen;
+    if (++G.arrived == G.world) {
+        G.arrived = 0;
+        ++G.gen;
+        G.cv.notify_all();
+        return;
+    }
+    // a rank that failed never arrives: fail instead of hanging the others
+    if (!G.cv.wait_for(l, std::chrono::seconds(300), [&] { return G.gen != my; }))
+        throw Err{HYT_ENCCL, "in-process group: barrier timed out (a rank failed?)"};
+}
+
+enum RedOp { RED_MIN_U32, RED_SUM_F32, RED_SUM_U64 };
+
+static void local_allreduce(hyt_graph *g, void *buf, uint64_t n, RedOp op, cudaStream_t st) {
+    LocalGroup &G = *static_cast<LocalGroup *>(g->local_group);
+    const uint64_t esz = op == RED_SUM_U64 ? 8 : 4, bytes = n * esz;
+    HYT_CUDA(cudaStreamSynchronize(st));
+    G.slot[g->rank].resize(bytes);
+    HYT_CUDA(cudaMemcpy(G.slot[g->rank].data(), buf, bytes, cudaMemcpyDeviceToHost));
+    local_barrier(G);
+    if (g->rank == 0) {    // reduce in rank order (a fixed order: f32 sums are reproducible)
+        G.result = G.slot[0];
+        for (int r = 1; r < G.world; ++r) {
+            const uint8_t *x = G.slot[r].data();
+            uint8_t *y = G.result.data();
+            for (uint64_t i = 0; i < n; ++i) {
+                if (op == RED_MIN_U32) {
+                    uint32_t a, b; std::memcpy(&a, y + 4 * i, 4); std::memcpy(&b, x + 4 * i, 4);
+                    if (b < a) std::memcpy(y + 4 * i, &b, 4);
+                } else if (op == RED_SUM_F32) {
+                    float a, b; std::memcpy(&a, y + 4 * i, 4); std::memcpy(&b, x + 4 * i, 4);
+                    a += b; std::memcpy(y + 4 * i, &a, 4);
+                } else {
+                    uint64_t a, b; std::memcpy(&a, y + 8 * i, 8); std::memcpy(&b, x + 8 * i, 8);
+                    a += b; std::memcpy(y + 8 * i, &a, 8);
+                }
+            }
+        }
+    }
+    local_barrier(G);
+    HYT_CUDA(cudaMemcpy(buf, G.result.data(), bytes, cudaMemcpyHostToDevice));
+    local_barrier(G);      // nobody starts the next reduction before all have read this one
+}
+
+void dist_init_local(hyt_graph *g, int rank, int world, uint64_t group) {
+    std::lock_guard<std::mutex> l(g_groups_mu);
+    auto &sp = g_groups[group];
+    if (!sp) {
+        sp = std::make_shared<LocalGroup>();
+        sp->world = world;
+        sp->slot.resize(world);
+    }
+    HYT_REQUIRE(sp->world == world, HYT_EINVAL, "in-process group: world size mismatch");
+    HYT_REQUIRE(sp->members < world, HYT_EINVAL, "in-process group: more members than world");
+    ++sp->members;
+    g->rank = rank;
+    g->world = world;
+    g->local_group = sp.get();
+    g->local_key = group;
+}
+
 void dist_init(hyt_graph *g, int rank, int world, const void *uid) {
     g->rank = rank;
     g->world = world;
@@ -68,18 +158,27 @@ void dist_init(hyt_graph *g, int rank, int world, const void *uid) {
 }
 
 void dist_allreduce_min_u32(hyt_graph *g, uint32_t *buf, uint64_t n, cudaStream_t st) {
+    if (g->local_group) return local_allreduce(g, buf, n, RED_MIN_U32, st);
     HYT_NCCL(nccl().AllReduce(buf, buf, n, ncclUint32, ncclMin, g->nccl_comm, st));
 }
 void dist_allreduce_sum_f32(hyt_graph *g, float *buf, uint64_t n, cudaStream_t st) {
+    if (g->local_group) return local_allreduce(g, buf, n, RED_SUM_F32, st);
     HYT_NCCL(nccl().AllReduce(buf, buf, n, ncclFloat32, ncclSum, g->nccl_comm, st));
 }
 void dist_allreduce_sum_u64(hyt_graph *g, uint64_t *buf, uint64_t n, cudaStream_t st) {
+    if (g->local_group) return local_allreduce(g, buf, n, RED_SUM_U64, st);
     HYT_NCCL(nccl().AllReduce(buf, buf, n, ncclUint64, ncclSum, g->nccl_comm, st));
 }
 void dist_free(hyt_graph *g) {
     if (g->nccl_comm) {
         nccl().CommDestroy(g->nccl_comm);
         g->nccl_comm = nullptr;
+    }
+    if (g->local_group) {
+        std::lock_guard<std::mutex> l(g_groups_mu);
+        auto it = g_groups.find(g->local_key);
+        if (it != g_groups.end() && --it->second->members == 0) g_groups.erase(it);
+        g->local_group = nullptr;
     }
 }
 

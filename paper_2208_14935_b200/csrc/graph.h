@@ -135,6 +135,8 @@ struct hyt_graph {
     // ---- multi-GPU ----
     int rank = 0, world = 1;
     void *nccl_comm = nullptr;
+    void *local_group = nullptr;   // in-process group (hyt_init_dist_local) instead of NCCL
+    uint64_t local_key = 0;
 };
 
 namespace hyt {
@@ -154,6 +156,7 @@ void rank_partitions(const std::vector<uint64_t> &off, const std::vector<uint64_
                      uint64_t *p_lo, uint64_t *p_hi);
 // multi-GPU exchange (dist.cu)
 void dist_init(hyt_graph *g, int rank, int world, const void *uid);
+void dist_init_local(hyt_graph *g, int rank, int world, uint64_t group);
 void dist_allreduce_min_u32(hyt_graph *g, uint32_t *buf, uint64_t n, cudaStream_t st);
 void dist_allreduce_sum_f32(hyt_graph *g, float *buf, uint64_t n, cudaStream_t st);
 void dist_allreduce_sum_u64(hyt_graph *g, uint64_t *buf, uint64_t n, cudaStream_t st);

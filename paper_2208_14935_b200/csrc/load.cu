@@ -235,43 +235,66 @@ static void parallel_memcpy(void *dst, const void *src, uint64_t bytes) {
 
 // Maps a caller host array for device reads: cudaHostRegister in place, or a
 // temporary pinned copy if registration is refused.
+// Registrations of caller arrays are reference-counted process-wide: several
+// handles (e.g. the ranks of an in-process group) may load from the same arrays
+// at once, and the first to finish must not unregister memory another is reading.
+static std::mutex g_reg_mu;
+struct RegEntry { uint64_t bytes; int refs; const void *dev; };
+static std::unordered_map<const void *, RegEntry> g_reg;
+
 struct HostView {
     const void *dev = nullptr;
-    void *reg = nullptr;        // registered base (to unregister)
+    const void *reg = nullptr;  // registry key (registered by us, refcounted)
     void *tmp = nullptr;        // pinned copy (to free)
     void open(const void *p, uint64_t bytes) {
         if (!p || bytes == 0) return;
+        std::lock_guard<std::mutex> l(g_reg_mu);
+        auto it = g_reg.find(p);
+        if (it != g_reg.end() && it->second.bytes >= bytes) {
+            ++it->second.refs;
+            reg = p;
+            dev = it->second.dev;
+            return;
+        }
         cudaError_t e = cudaHostRegister((void *)p, bytes, cudaHostRegisterMapped | cudaHostRegisterReadOnly);
         if (e != cudaSuccess) {
             cudaGetLastError();
             e = cudaHostRegister((void *)p, bytes, cudaHostRegisterMapped);
         }
         if (e == cudaSuccess) {
-            reg = (void *)p;
-        } else {
-            cudaGetLastError();
-            cudaPointerAttributes at{};
-            if (e == cudaErrorHostMemoryAlreadyRegistered &&
-                cudaPointerGetAttributes(&at, p) == cudaSuccess && at.devicePointer) {
-                dev = at.devicePointer;
-                return;
-            }
-            cudaGetLastError();
-            HYT_CUDA(cudaHostAlloc(&tmp, bytes, cudaHostAllocMapped));
-            parallel_memcpy(tmp, p, bytes);
             void *d = nullptr;
-            HYT_CUDA(cudaHostGetDevicePointer(&d, tmp, 0));
+            HYT_CUDA(cudaHostGetDevicePointer(&d, (void *)p, 0));
+            g_reg[p] = RegEntry{bytes, 1, d};
+            reg = p;
             dev = d;
             return;
         }
+        cudaGetLastError();
+        cudaPointerAttributes at{};
+        if (e == cudaErrorHostMemoryAlreadyRegistered && cudaPointerGetAttributes(&at, p) == cudaSuccess &&
+            at.devicePointer) {
+            dev = at.devicePointer;         // registered by the caller: theirs to release
+            return;
+        }
+        cudaGetLastError();
+        HYT_CUDA(cudaHostAlloc(&tmp, bytes, cudaHostAllocMapped));
+        parallel_memcpy(tmp, p, bytes);
         void *d = nullptr;
-        HYT_CUDA(cudaHostGetDevicePointer(&d, (void *)p, 0));
+        HYT_CUDA(cudaHostGetDevicePointer(&d, tmp, 0));
         dev = d;
     }
     void close() {
-        if (reg) cudaHostUnregister(reg);
+        if (reg) {
+            std::lock_guard<std::mutex> l(g_reg_mu);
+            auto it = g_reg.find(reg);
+            if (it != g_reg.end() && --it->second.refs == 0) {
+                cudaHostUnregister((void *)reg);
+                g_reg.erase(it);
+            }
+        }
         if (tmp) cudaFreeHost(tmp);
-        reg = tmp = nullptr;
+        reg = nullptr;
+        tmp = nullptr;
         dev = nullptr;
     }
 };

@@ -1,0 +1,97 @@
+"""GPU parity of the multi-rank path on one device.
+
+`world` handles, one per thread, join an in-process group (hyt_init_dist_local):
+the same vertex-range split, per-iteration reductions (min for BFS/SSSP/CC, sum for
+PR deltas and ranks), owner-side frontier merge and global termination as a NCCL
+job, with the reductions carried through host memory.  Every rank's gathered
+result must equal the oracle's: bit-exact for BFS/SSSP/CC, 1e-4 relative for PR."""
+import itertools
+import threading
+
+import numpy as np
+import pytest
+
+from test_gpu_parity import CRAFTED, assert_pr_close, expected, gkey_graph, src_of, symmetric_version
+
+pytestmark = pytest.mark.gpu
+
+_group = itertools.count(1000)
+
+
+def run_ranks(hyt, g, algo, world, engine="hybrid", part=4096, budget=0, **kw):
+    key = next(_group)
+    out, err = [None] * world, [None] * world
+
+    def body(r):
+        G = None
+        try:
+            G = hyt.Graph(device=0, budget=budget)
+            G.init_dist_local(r, world, key)
+            G.load(g.off, g.nbr, g.w)
+            G.set("engine_mode", engine)
+            G.set("partition_bytes", part)
+            for k, v in kw.items():
+                G.set(k, v)
+            G.run(algo, src_of(g) if algo in ("bfs", "sssp") else 0)
+            out[r] = (G.values(), G.stats())
+        except Exception as e:          # noqa: BLE001 -- re-raised in the main thread
+            err[r] = e
+        finally:
+            if G is not None:
+                G.close()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    assert all(o is not None for o in out)
+    return out
+
+
+def check(gkey, algo, outs):
+    want = expected(gkey, algo)
+    for vals, _ in outs:
+        if algo == "pr":
+            assert_pr_close(vals, want)
+        else:
+            assert np.array_equal(vals, want)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("engine", ["hybrid", "filter", "compaction", "zerocopy", "resident"])
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+@pytest.mark.parametrize("gi", [4, 9])
+def test_multirank_engines(hyt, world, engine, algo, gi):
+    gkey = ("rmat", gi)
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    outs = run_ranks(hyt, g, algo, world, engine=engine)
+    check(gkey, algo, outs)
+    # the ranks agree on the iteration count (global termination)
+    assert len({st["iterations"] for _, st in outs}) == 1
+
+
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+@pytest.mark.parametrize("ci", range(len(CRAFTED)))
+def test_multirank_crafted(hyt, algo, ci):
+    """Crafted graphs at world 4: stars whose hub holds more than E/world edges
+    (ranks without vertices), chains, isolated vertices, the empty edge set."""
+    gkey = ("crafted", ci)
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    outs = run_ranks(hyt, g, algo, 4)
+    check(gkey, algo, outs)
+
+
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "pr"])
+def test_multirank_budget_and_cache(hyt, algo):
+    """Per-rank device budget with the partial edge cache: each rank caches a prefix
+    of its own partitions."""
+    gkey = ("rmat", 13)
+    g = gkey_graph(gkey)
+    d1 = 8 if algo == "sssp" else 4
+    outs = run_ranks(hyt, g, algo, 2, part=4096, edge_cache=1, edge_cache_bytes=g.E * d1 // 4)
+    check(gkey, algo, outs)
+    assert sum(st["parts_resident"] for _, st in outs) > 0
