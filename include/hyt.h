@@ -232,10 +232,12 @@ int hyt_select_engine(const hyt_graph *g, uint64_t t, uint64_t e, uint64_t a, ui
 /* ---- multi-GPU (vertex-range sharding, NCCL over NVLink) ----
  * Call after hyt_init and before hyt_load_csr on every rank.  nccl_uid is the
  * 128-byte ncclUniqueId created by rank 0 (hyt_nccl_unique_id) and broadcast
- * by the caller (e.g. torch.distributed).  Every rank then loads the SAME
- * graph; each rank serves its own contiguous range of partitions and the
- * ranks exchange pushed values once per iteration (min for BFS/SSSP/CC, sum
- * for PR deltas).  Errors: HYT_ENCCL. */
+ * by the caller (e.g. torch.distributed).  Every rank then passes the SAME
+ * graph to hyt_load_csr.  Each rank computes the same hub order and keeps in
+ * pinned host memory only the edges of its own vertex range, about E/world of
+ * them (hyt_rank_range).  It serves the partitions of that range.  Once per
+ * iteration the ranks exchange pushed values: min for BFS/SSSP/CC, sum for PR
+ * deltas.  Errors: HYT_ENCCL. */
 int hyt_nccl_unique_id(void *uid_out_128_bytes);
 int hyt_init_dist(hyt_graph *g, int rank, int world, const void *nccl_uid_128_bytes);
 
@@ -248,12 +250,16 @@ int hyt_init_dist(hyt_graph *g, int rank, int world, const void *nccl_uid_128_by
 int hyt_init_dist_local(hyt_graph *g, int rank, int world, uint64_t group);
 
 /* The vertex-range split of a multi-GPU job (host routine the library uses,
- * exposed for CPU tests): with the greedy partitions of `partition_bytes` at
- * record width d1 over off_host (u64[V+1], the graph as loaded), rank `rank` of
- * `world` owns partitions [*p_lo, *p_hi) = vertices [*v_lo, *v_hi): contiguous
- * runs with about E/world edges each (cut where the edge prefix crosses
- * r*E/world).  Returns the total partition count (>= 0) or HYT_EINVAL.
- * Needs no GPU. */
+ * exposed for CPU tests).  off_host is u64[V+1], the graph as loaded.  Rank r
+ * of `world` owns vertices [*v_lo, *v_hi) = [R_r, R_(r+1)), where R_r is the
+ * first vertex whose edge offset reaches r*E/world and R_world = V.  A rank's
+ * edge count is therefore within the largest out-degree of E/world; a rank
+ * may own no vertex when one vertex holds more than E/world edges.  Inside
+ * each rank's range, partitions are the greedy `partition_bytes` sweep at
+ * record width d1, so no partition crosses a rank cut.  Rank r owns
+ * partitions [*p_lo, *p_hi).  The split does not depend on d1 or
+ * partition_bytes, so one pinned edge store per rank serves every algorithm.
+ * Returns the total partition count (>= 0) or HYT_EINVAL.  Needs no GPU. */
 int64_t hyt_rank_range(const uint64_t *off_host, uint64_t V, uint64_t d1, uint64_t partition_bytes, int world,
                        int rank, uint64_t *p_lo, uint64_t *p_hi, uint64_t *v_lo, uint64_t *v_hi);
 

@@ -192,7 +192,7 @@ int64_t hyt_rank_range(const uint64_t *off, uint64_t V, uint64_t d1, uint64_t pa
     }
     try {
         std::vector<uint64_t> o(off, off + V + 1);
-        std::vector<uint64_t> b = partition_bounds(o, d1, partition_bytes);
+        std::vector<uint64_t> b = partition_bounds_ranked(o, d1, partition_bytes, world);
         rank_partitions(o, b, world, rank, p_lo, p_hi);
         *v_lo = b[*p_lo];
         *v_hi = b[*p_hi];

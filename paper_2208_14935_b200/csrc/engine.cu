@@ -101,19 +101,45 @@ CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio, double zr_r
 // ---------------------------------------------------------------------------
 // host partitioner and task combination
 // ---------------------------------------------------------------------------
-std::vector<uint64_t> partition_bounds(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target) {
-    // greedy sweep (close a partition when the next vertex would exceed target,
-    // unless empty), realised by binary search on the offsets.
-    const uint64_t V = off.size() - 1;
-    std::vector<uint64_t> b{0};
-    uint64_t lo = 0;
-    while (lo < V) {
+static void greedy_bounds(const std::vector<uint64_t> &off, uint64_t lo, uint64_t end, uint64_t d1, uint64_t target,
+                          std::vector<uint64_t> &b) {
+    // greedy sweep over [lo, end) (close a partition when the next vertex would
+    // exceed target, unless empty), realised by binary search on the offsets
+    while (lo < end) {
         // largest hi with (off[hi] - off[lo]) * d1 <= target, at least lo + 1
         const uint64_t lim = off[lo] + target / d1;
-        uint64_t hi = std::upper_bound(off.begin() + lo + 1, off.end(), lim) - off.begin() - 1;
+        uint64_t hi = std::upper_bound(off.begin() + lo + 1, off.begin() + end + 1, lim) - off.begin() - 1;
         if (hi <= lo) hi = lo + 1;
         b.push_back(hi);
         lo = hi;
+    }
+}
+
+std::vector<uint64_t> partition_bounds(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target) {
+    std::vector<uint64_t> b{0};
+    greedy_bounds(off, 0, off.size() - 1, d1, target, b);
+    return b;
+}
+
+void rank_vertex_range(const std::vector<uint64_t> &off, int world, int rank, uint64_t *v_lo, uint64_t *v_hi) {
+    const uint64_t V = off.size() - 1, E = off[V];
+    auto cut = [&](int r) -> uint64_t {
+        if (r <= 0) return 0;
+        if (r >= world) return V;
+        const uint64_t target = (uint64_t)((unsigned __int128)E * (uint64_t)r / (uint64_t)world);
+        return std::lower_bound(off.begin(), off.end() - 1, target) - off.begin();
+    };
+    *v_lo = cut(rank);
+    *v_hi = std::max(*v_lo, cut(rank + 1));
+}
+
+std::vector<uint64_t> partition_bounds_ranked(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target,
+                                              int world) {
+    std::vector<uint64_t> b{0};
+    for (int r = 0; r < world; ++r) {
+        uint64_t lo, hi;
+        rank_vertex_range(off, world, r, &lo, &hi);
+        greedy_bounds(off, lo, hi, d1, target, b);
     }
     return b;
 }
@@ -135,22 +161,17 @@ int64_t combine_units(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units)
 
 void rank_partitions(const std::vector<uint64_t> &off, const std::vector<uint64_t> &bounds, int world, int rank,
                      uint64_t *p_lo, uint64_t *p_hi) {
-    const uint64_t N = bounds.size() - 1, V = off.size() - 1, E = off[V];
-    auto cut = [&](int r) -> uint64_t {
-        if (r <= 0) return 0;
-        if (r >= world) return N;
-        const uint64_t target = (uint64_t)((unsigned __int128)E * (uint64_t)r / (uint64_t)world);
-        // first partition whose starting edge offset reaches the target
-        uint64_t lo = 0, hi = N;
-        while (lo < hi) {
-            const uint64_t mid = (lo + hi) / 2;
-            if (off[bounds[mid]] < target) lo = mid + 1; else hi = mid;
-        }
-        return lo;
-    };
-    *p_lo = cut(rank);
-    *p_hi = cut(rank + 1);
-    if (*p_hi < *p_lo) *p_hi = *p_lo;
+    // bounds from partition_bounds_ranked: every rank cut is a partition bound
+    uint64_t lo, hi;
+    rank_vertex_range(off, world, rank, &lo, &hi);
+    *p_lo = std::lower_bound(bounds.begin(), bounds.end(), lo) - bounds.begin();
+    *p_hi = std::lower_bound(bounds.begin(), bounds.end(), hi) - bounds.begin();
+}
+
+const uint4 *host_edges(const hyt_graph *g, uint32_t d1) {
+    const int i = d1 == 8 ? 1 : 0;
+    const uintptr_t base = (uintptr_t)(i ? (const void *)g->ew_h : (const void *)g->nbr_h);
+    return (const uint4 *)(base - g->store_c0[i] * 16);
 }
 
 // ---------------------------------------------------------------------------
@@ -325,8 +346,7 @@ static void fill_cache(hyt_graph *g, RunCtx *c, uint64_t p_hi_cache) {
     const uint64_t c0 = chunk_lo(g->off_h[c->bounds[c->p_lo]], c->d1);
     const uint64_t c1 = chunk_hi(g->off_h[c->bounds[p_hi_cache]], c->d1);
     c->cache = dalloc<uint4>(g, c, c1 - c0 + 1, "resident edge cache");
-    const uint4 *src = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
-    HYT_CUDA(cudaMemcpy(c->cache, src + c0, (c1 - c0) * 16, cudaMemcpyHostToDevice));
+    HYT_CUDA(cudaMemcpy(c->cache, host_edges(g, c->d1) + c0, (c1 - c0) * 16, cudaMemcpyHostToDevice));
     c->cache_c0 = c0;
     c->cache_hi = p_hi_cache;
     c->cache_bytes = (c1 - c0) * 16;
@@ -339,9 +359,9 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->algo = algo;
         c->d1 = (algo == ALGO_SSSP) ? 8 : 4;
         const uint64_t V = g->V, W = (V + 31) / 32;
-        c->bounds = partition_bounds(g->off_h, c->d1, P.partition_bytes);
+        c->bounds = partition_bounds_ranked(g->off_h, c->d1, P.partition_bytes, g->world);
         c->N = c->bounds.size() - 1;
-        // ---- multi-GPU: contiguous run of partitions with ~equal edge bytes ----
+        // ---- multi-GPU: the partitions of this rank's vertex range (~E/world edges) ----
         rank_partitions(g->off_h, c->bounds, g->world, g->rank, &c->p_lo, &c->p_hi);
         c->v_lo = c->bounds[c->p_lo];
         c->v_hi = c->bounds[c->p_hi];
@@ -670,14 +690,14 @@ static void calibrate(hyt_graph *g, RunCtx *c) {
         }
     }
     if (P.thpt_cpt_gbs > 0) g->est_cpt_gbs = P.thpt_cpt_gbs;
-    const uint4 *edges_host = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
-    if (g->est_cpt_gbs <= 0 && c->pool && c->cq_cap > 1) {
-        // the lists of up to 64K random vertices with out-edges, gathered like the C engine
+    const uint4 *edges_host = host_edges(g, c->d1);
+    if (g->est_cpt_gbs <= 0 && c->pool && c->cq_cap > 1 && c->v_hi > c->v_lo) {
+        // the lists of up to 64K random own vertices with out-edges, gathered like the C engine
         std::vector<uint32_t> vs;
         uint64_t x = 0x9E3779B97F4A7C15ull;
         for (uint64_t tries = 0; vs.size() < 65536 && tries < 1000000; ++tries) {
             x ^= x << 13; x ^= x >> 7; x ^= x << 17;
-            const uint64_t v = x % g->V;
+            const uint64_t v = c->v_lo + x % (c->v_hi - c->v_lo);
             if (g->off_h[v + 1] > g->off_h[v]) vs.push_back((uint32_t)v);
         }
         const uint64_t n = std::min<uint64_t>(vs.size(), c->cq_cap);
@@ -734,9 +754,11 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     const int prio = P.priority >= 0 ? P.priority : (algo == ALGO_PR ? 2 : 1);
     const int sms = 148;
     const int relax_ctas = sms * P.relax_ctas_per_sm, zc_ctas = sms * P.zc_ctas_per_sm;
-    const uint4 *edges_host = (const uint4 *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h);
-    const uint4 *edges_mapped = nullptr;
-    HYT_CUDA(cudaHostGetDevicePointer((void **)&edges_mapped, (void *)edges_host, 0));
+    const uint4 *edges_host = host_edges(g, c->d1);          // indexed by global chunk
+    const uint64_t store_c0 = g->store_c0[c->d1 == 8 ? 1 : 0];
+    const uint4 *edges_mapped = nullptr;                       // device view of the store's first chunk
+    HYT_CUDA(cudaHostGetDevicePointer((void **)&edges_mapped,
+                                      (void *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h), 0));
 
     // reset statistics
     g->stats = hyt_stats{};
@@ -876,7 +898,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             cudaStream_t stm = g->st[c->S];
             EvPair e1;
             timed_begin(c, stm, e1, TAG_Z);
-            EdgeSrc es{edges_mapped, 0, false};
+            EdgeSrc es{edges_mapped, (int64_t)store_c0, false};
             if (algo == ALGO_PR) {
                 launch_take_delta(s, c->q, H.ent_base[ENG_Z], H.ent_base[ENG_Z] + H.ent_count[ENG_Z], stm);
                 g->launches += 1;
@@ -1059,7 +1081,7 @@ void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_par
     HYT_REQUIRE(algo >= ALGO_BFS && algo <= ALGO_PR, HYT_EINVAL, "unknown algorithm");
     HYT_CUDA(cudaSetDevice(g->device));
     const uint32_t d1 = algo == ALGO_SSSP ? 8 : 4;
-    std::vector<uint64_t> b = partition_bounds(g->off_h, d1, g->prm.partition_bytes);
+    std::vector<uint64_t> b = partition_bounds_ranked(g->off_h, d1, g->prm.partition_bytes, g->world);
     const uint64_t N = b.size() - 1;
     *num_parts = N;
     if (!bounds && !t && !p) return;

@@ -106,8 +106,14 @@ struct hyt_graph {
     bool loaded = false;
     uint64_t V = 0, E = 0;
     bool weighted = false;
-    uint32_t *nbr_h = nullptr;      // pinned mapped u32[E] (+pad)
-    uint64_t *ew_h = nullptr;       // pinned mapped (id | w<<32) u64[E] (+pad), weighted only
+    // Edge store: pinned mapped records of this rank's vertex range only
+    // [store_v_lo, store_v_hi) (the whole graph when world == 1), starting at the
+    // 16-byte chunk store_c0[0] (u32 ids) / store_c0[1] (id | w<<32) of the global
+    // edge byte space.  host_edges() returns pointers indexed by GLOBAL chunk.
+    uint32_t *nbr_h = nullptr;      // pinned mapped u32 ids (+pad)
+    uint64_t *ew_h = nullptr;       // pinned mapped (id | w<<32) u64 (+pad), weighted only
+    uint64_t store_v_lo = 0, store_v_hi = 0;
+    uint64_t store_c0[2] = {0, 0};
     std::vector<uint64_t> off_h;    // host copy of offsets u64[V+1]
     uint64_t *off_d = nullptr;      // device offsets
     uint32_t *new_id_d = nullptr;   // caller id -> internal id
@@ -151,9 +157,16 @@ void release_run_ctx(hyt_graph *g);   // drop cached run buffers (parameters cha
 // host partitioner: greedy 32-MiB sweep by binary search on offsets
 std::vector<uint64_t> partition_bounds(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target);
 int64_t combine_units(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units);
-// contiguous run of partitions owned by `rank` (about E/world edges each)
+// multi-GPU split: rank r owns vertices [R_r, R_r+1), R_r = the first vertex whose
+// edge offset reaches r*E/world (R_world = V); partitions never cross a rank cut
+void rank_vertex_range(const std::vector<uint64_t> &off, int world, int rank, uint64_t *v_lo, uint64_t *v_hi);
+std::vector<uint64_t> partition_bounds_ranked(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target,
+                                              int world);
 void rank_partitions(const std::vector<uint64_t> &off, const std::vector<uint64_t> &bounds, int world, int rank,
                      uint64_t *p_lo, uint64_t *p_hi);
+// host pointer to the edge store of record width d1, indexed by GLOBAL 16-byte
+// chunk (valid for the chunks of the store's vertex range only)
+const uint4 *host_edges(const hyt_graph *g, uint32_t d1);
 // multi-GPU exchange (dist.cu)
 void dist_init(hyt_graph *g, int rank, int world, const void *uid);
 void dist_init_local(hyt_graph *g, int rank, int world, uint64_t group);

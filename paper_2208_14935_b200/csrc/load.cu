@@ -166,17 +166,20 @@ __global__ void k_finish_perm(uint64_t V, uint64_t h, const uint32_t *__restrict
 constexpr int kRelabelTile = 8192, kRelabelRows = 2048;
 
 __global__ void __launch_bounds__(512)
-k_relabel_tiles(uint64_t V, uint64_t E, const uint64_t *__restrict__ off_old, const uint64_t *__restrict__ off_new,
+k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__restrict__ off_old,
+                const uint64_t *__restrict__ off_new,
                 const uint32_t *__restrict__ old_of, const uint32_t *__restrict__ new_id,
                 const uint32_t *__restrict__ nbr_in, const uint32_t *__restrict__ w_in,
                 uint32_t *__restrict__ nbr_out, uint64_t *__restrict__ ew_out) {
     __shared__ uint64_t s_new[kRelabelRows + 1];
     __shared__ uint64_t s_old[kRelabelRows];
     __shared__ uint64_t s_r0;
-    const uint64_t ntiles = (E + kRelabelTile - 1) / kRelabelTile;
+    // edges [e_lo, e_hi) of the new order; nbr_out / ew_out are indexed by the
+    // global edge index (the caller offsets them to its store's first record)
+    const uint64_t ntiles = (e_hi - e_lo + kRelabelTile - 1) / kRelabelTile;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        uint64_t e = t * kRelabelTile;
-        const uint64_t e_end = min(E, e + kRelabelTile);
+        uint64_t e = e_lo + t * kRelabelTile;
+        const uint64_t e_end = min(e_hi, e + kRelabelTile);
         while (e < e_end) {
             __syncthreads();
             if (threadIdx.x == 0) {        // last row whose start <= e (skips empty rows)
@@ -429,24 +432,31 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         HYT_CUDA(cudaMemcpyAsync(g->off_h.data(), g->off_d, (V + 1) * 8, cudaMemcpyDeviceToHost, st));
         phase("hub sort + new offsets");
 
-        // ---- pinned mapped edge store (16-B padded so chunk loads never overrun) ----
-        const uint64_t nbytes = ((E * 4 + 15) & ~15ull) + 32;
+        HYT_CUDA(cudaStreamSynchronize(st));   // off_h ready
+        // ---- pinned mapped edge store of this rank's vertex range (the
+        // whole graph at world 1), from a 16-byte chunk boundary, 16-B padded so chunk
+        // loads never overrun ----
+        rank_vertex_range(g->off_h, g->world, g->rank, &g->store_v_lo, &g->store_v_hi);
+        const uint64_t e_lo = g->off_h[g->store_v_lo], e_hi = g->off_h[g->store_v_hi];
+        g->store_c0[0] = e_lo / 4;                          // first chunk of u32 ids
+        g->store_c0[1] = e_lo / 2;                          // first chunk of u64 records
+        const uint64_t nbase = g->store_c0[0] * 4, wbase = g->store_c0[1] * 2;
+        const uint64_t nbytes = (((e_hi - nbase) * 4 + 15) & ~15ull) + 32;
         g->nbr_h = (uint32_t *)pinned_alloc(nbytes);      // zero-filled (padding included)
         if (w) {
-            const uint64_t wbytes = ((E * 8 + 15) & ~15ull) + 32;
+            const uint64_t wbytes = (((e_hi - wbase) * 8 + 15) & ~15ull) + 32;
             g->ew_h = (uint64_t *)pinned_alloc(wbytes);
         }
         uint32_t *nbr_out = nullptr;
         uint64_t *ew_out = nullptr;
         HYT_CUDA(cudaHostGetDevicePointer((void **)&nbr_out, g->nbr_h, 0));
         if (w) HYT_CUDA(cudaHostGetDevicePointer((void **)&ew_out, g->ew_h, 0));
-        HYT_CUDA(cudaStreamSynchronize(st));   // off_h ready
         phase("pin edge store");
 
-        if (E) {
-            k_relabel_tiles<<<148 * 4, 512, 0, st>>>(V, E, off_old, g->off_d, g->old_of_d, g->new_id_d,
-                                                      (const uint32_t *)vn.dev, (const uint32_t *)vw.dev, nbr_out,
-                                                      ew_out);
+        if (e_hi > e_lo) {
+            k_relabel_tiles<<<148 * 4, 512, 0, st>>>(V, e_lo, e_hi, off_old, g->off_d, g->old_of_d, g->new_id_d,
+                                                      (const uint32_t *)vn.dev, (const uint32_t *)vw.dev,
+                                                      nbr_out - nbase, ew_out ? ew_out - wbase : nullptr);
         }
         HYT_CUDA(cudaStreamSynchronize(st));
         HYT_CUDA(cudaGetLastError());

@@ -163,3 +163,33 @@ def test_gloo_pr_outbox_exchange_matches_oracle():
     want, _ = oracle.pr_jacobi(g.off, g.nbr)
     for rank, rr, r in out:
         assert np.max(np.abs(r - want) / want) < 1e-7
+
+
+def test_rank_split_independent_of_partitioning():
+    """The vertex-range split depends on the offsets only (one pinned edge store per
+    rank serves every algorithm and partition size), cuts at the first vertex whose
+    offset reaches r*E/world, and no partition crosses a cut."""
+    g = hytgen.rmat_csr(13, 8192, 120000, seed=5)
+    off = g.off.astype(np.int64)
+    for world in (2, 3, 8):
+        for r in range(world):
+            rs = [hyt.rank_range(g.off, d1, pb, world, r) for d1 in (4, 8) for pb in (4096, 65536, 32 << 20)]
+            assert len({(x["v_lo"], x["v_hi"]) for x in rs}) == 1
+            lo = rs[0]["v_lo"]
+            want = 0 if r == 0 else int(np.searchsorted(off, g.E * r // world, side="left"))
+            assert lo == want
+
+
+def test_rank_split_hub_larger_than_share():
+    """A star whose hub holds most edges: ranks past the hub's share own nothing,
+    the ranges still tile [0, V)."""
+    V = 1000
+    src = [0] * 900 + list(range(1, 100))
+    dst = list(range(1, 901)) + list(range(2, 101))
+    g = hytgen.csr_from_edges(V, src, dst, name="bighub")
+    world = 4
+    rs = [hyt.rank_range(g.off, 4, 4096, world, r) for r in range(world)]
+    assert rs[0]["v_lo"] == 0 and rs[-1]["v_hi"] == V
+    for a, b in zip(rs, rs[1:]):
+        assert a["v_hi"] == b["v_lo"] and a["p_hi"] == b["p_lo"]
+    assert any(x["v_hi"] == x["v_lo"] for x in rs)
