@@ -311,6 +311,7 @@ def main():
     eng_edges = np.zeros(8, dtype=np.int64)
     link_bytes = 0
     iters = {a: 0 for a in algos}
+    exch = {a: None for a in algos}
     detail = {}
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -330,6 +331,8 @@ def main():
                 eng_edges += np.array(st["eng_edges"])
                 link_bytes += st["bytes_filter"] + st["bytes_compaction"] + st["bytes_zerocopy"]
                 iters[a] = st["iterations"]
+                exch[a] = {"sparse_iters": st["exch_sparse"], "dense_iters": st["exch_dense"],
+                           "bytes_per_rank": st["exch_bytes"]}
                 if args.detail_out:
                     detail[a] = {"stats": st, "iter_log": G.iter_log()}
             barrier()
@@ -427,6 +430,8 @@ def main():
         ms = float(np.mean(per_algo_ms[a]))
         per_algo[a] = {"time_to_converge_s": ms / 1e3, "gteps": edges_per[a] / (ms / 1e3) / 1e9,
                        "edges": int(edges_per[a]), "iterations": int(iters[a])}
+        if world > 1:
+            per_algo[a]["exchange"] = exch[a]
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",

@@ -104,6 +104,10 @@ typedef struct {
      * DMA link GB/s, host gather GB/s (Thpt_cpt), zero-copy ns per random
      * 128-B request and per streamed 128-B line. */
     double   cal_link_gbs, cal_cpt_gbs, cal_zc_req_ns, cal_zc_line_ns;
+    /* multi-GPU exchange (world > 1): iterations that used the
+     * sparse pair all-gather / the dense V-entry reduction, and the payload
+     * bytes each rank contributed (pairs x 8 B, or V x 4 B). */
+    uint64_t exch_sparse, exch_dense, exch_bytes;
 } hyt_stats;
 
 /* One row per iteration (hyt_get_iter_log), the Fig. 7 / Table VI analog. */
@@ -177,6 +181,11 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   zc_ctas_per_sm [2], relax_minb [4] (__launch_bounds__ min CTAs/SM, 4..6),
  *   relax_hot [1] (hub block ids < 4096 in shared memory: PR delta
  *   accumulation, min-algorithm value copy; 0 off, 1 auto, 2 always).
+ *   exchange [1] (world > 1): 0 always the dense V-entry
+ *   all-reduce; 1 per iteration, all-gather the (id, value) pairs each rank
+ *   changed when their bytes (world x max pairs x 8) are below the dense
+ *   payload (V x 4), else dense; 2 sparse whenever the pairs fit the buffer.
+ *   Results are the same either way.
  * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
 int hyt_set_param(hyt_graph *g, const char *key, double value);
 

@@ -23,13 +23,14 @@ namespace hyt {
 typedef struct { char internal[128]; } nccl_uid_t;
 typedef void *nccl_comm_t;
 enum { ncclUint32 = 3, ncclUint64 = 5, ncclFloat32 = 7 };
-enum { ncclSum = 0, ncclMin = 3 };
+enum { ncclSum = 0, ncclMax = 2, ncclMin = 3 };
 
 struct NcclApi {
     void *h = nullptr;
     int (*GetUniqueId)(nccl_uid_t *) = nullptr;
     int (*CommInitRank)(nccl_comm_t *, int, nccl_uid_t, int) = nullptr;
     int (*AllReduce)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    int (*AllGather)(const void *, void *, size_t, int, nccl_comm_t, cudaStream_t) = nullptr;
     int (*CommDestroy)(nccl_comm_t) = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
 };
@@ -50,9 +51,10 @@ static NcclApi &nccl() {
         api.GetUniqueId = (int (*)(nccl_uid_t *))dlsym(api.h, "ncclGetUniqueId");
         api.CommInitRank = (int (*)(nccl_comm_t *, int, nccl_uid_t, int))dlsym(api.h, "ncclCommInitRank");
         api.AllReduce = (int (*)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t))dlsym(api.h, "ncclAllReduce");
+        api.AllGather = (int (*)(const void *, void *, size_t, int, nccl_comm_t, cudaStream_t))dlsym(api.h, "ncclAllGather");
         api.CommDestroy = (int (*)(nccl_comm_t))dlsym(api.h, "ncclCommDestroy");
         api.GetErrorString = (const char *(*)(int))dlsym(api.h, "ncclGetErrorString");
-        HYT_REQUIRE(api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy, HYT_ENCCL,
+        HYT_REQUIRE(api.GetUniqueId && api.CommInitRank && api.AllReduce && api.AllGather && api.CommDestroy, HYT_ENCCL,
                     "libnccl is missing symbols");
     }
     return api;
@@ -95,11 +97,11 @@ static void local_barrier(LocalGroup &G) {
         throw Err{HYT_ENCCL, "in-process group: barrier timed out (a rank failed?)"};
 }
 
-enum RedOp { RED_MIN_U32, RED_SUM_F32, RED_SUM_U64 };
+enum RedOp { RED_MIN_U32, RED_SUM_F32, RED_SUM_U64, RED_MAX_U64 };
 
 static void local_allreduce(hyt_graph *g, void *buf, uint64_t n, RedOp op, cudaStream_t st) {
     LocalGroup &G = *static_cast<LocalGroup *>(g->local_group);
-    const uint64_t esz = op == RED_SUM_U64 ? 8 : 4, bytes = n * esz;
+    const uint64_t esz = (op == RED_SUM_U64 || op == RED_MAX_U64) ? 8 : 4, bytes = n * esz;
     HYT_CUDA(cudaStreamSynchronize(st));
     G.slot[g->rank].resize(bytes);
     HYT_CUDA(cudaMemcpy(G.slot[g->rank].data(), buf, bytes, cudaMemcpyDeviceToHost));
@@ -118,7 +120,8 @@ static void local_allreduce(hyt_graph *g, void *buf, uint64_t n, RedOp op, cudaS
                     a += b; std::memcpy(y + 4 * i, &a, 4);
                 } else {
                     uint64_t a, b; std::memcpy(&a, y + 8 * i, 8); std::memcpy(&b, x + 8 * i, 8);
-                    a += b; std::memcpy(y + 8 * i, &a, 8);
+                    a = op == RED_SUM_U64 ? a + b : (b > a ? b : a);
+                    std::memcpy(y + 8 * i, &a, 8);
                 }
             }
         }
@@ -126,6 +129,19 @@ static void local_allreduce(hyt_graph *g, void *buf, uint64_t n, RedOp op, cudaS
     local_barrier(G);
     HYT_CUDA(cudaMemcpy(buf, G.result.data(), bytes, cudaMemcpyHostToDevice));
     local_barrier(G);      // nobody starts the next reduction before all have read this one
+}
+
+// recv = the ranks' send buffers concatenated in rank order (n u32 each)
+static void local_allgather(hyt_graph *g, const void *send, void *recv, uint64_t n, cudaStream_t st) {
+    LocalGroup &G = *static_cast<LocalGroup *>(g->local_group);
+    const uint64_t bytes = n * 4;
+    HYT_CUDA(cudaStreamSynchronize(st));
+    G.slot[g->rank].resize(bytes);
+    HYT_CUDA(cudaMemcpy(G.slot[g->rank].data(), send, bytes, cudaMemcpyDeviceToHost));
+    local_barrier(G);
+    for (int r = 0; r < G.world; ++r)
+        HYT_CUDA(cudaMemcpy((uint8_t *)recv + (uint64_t)r * bytes, G.slot[r].data(), bytes, cudaMemcpyHostToDevice));
+    local_barrier(G);
 }
 
 void dist_init_local(hyt_graph *g, int rank, int world, uint64_t group) {
@@ -168,6 +184,14 @@ void dist_allreduce_sum_f32(hyt_graph *g, float *buf, uint64_t n, cudaStream_t s
 void dist_allreduce_sum_u64(hyt_graph *g, uint64_t *buf, uint64_t n, cudaStream_t st) {
     if (g->local_group) return local_allreduce(g, buf, n, RED_SUM_U64, st);
     HYT_NCCL(nccl().AllReduce(buf, buf, n, ncclUint64, ncclSum, g->nccl_comm, st));
+}
+void dist_allreduce_max_u64(hyt_graph *g, uint64_t *buf, uint64_t n, cudaStream_t st) {
+    if (g->local_group) return local_allreduce(g, buf, n, RED_MAX_U64, st);
+    HYT_NCCL(nccl().AllReduce(buf, buf, n, ncclUint64, ncclMax, g->nccl_comm, st));
+}
+void dist_allgather_u32(hyt_graph *g, const uint32_t *send, uint32_t *recv, uint64_t n, cudaStream_t st) {
+    if (g->local_group) return local_allgather(g, send, recv, n, st);
+    HYT_NCCL(nccl().AllGather(send, recv, n, ncclUint32, g->nccl_comm, st));
 }
 void dist_free(hyt_graph *g) {
     if (g->nccl_comm) {

@@ -261,6 +261,12 @@ struct RunCtx {
     uint64_t *cq_pre = nullptr;
     uint64_t cq_cap = 0;
     uint32_t *snap = nullptr;     // multi-GPU: own-range values before the exchange
+    // multi-GPU sparse exchange (§8f #3): full values at iteration start (min-algos),
+    // own changed pairs, all ranks' pairs, own pair count
+    uint32_t *snapfull = nullptr;
+    uint2 *xsend = nullptr, *xrecv = nullptr;
+    uint64_t xcap = 0;
+    unsigned long long *xcnt = nullptr;
     uint64_t *red = nullptr;      // multi-GPU: device scratch for the active-count reduction
     uint64_t *racc = nullptr;     // recompute statistics accumulators (u64[4])
     uint32_t *outbuf = nullptr;   // u32[V] result staging for hyt_get_values
@@ -370,6 +376,14 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->outbuf = dalloc<uint32_t>(g, c, V, "result staging");
         if (g->world > 1 && algo != ALGO_PR)
             c->snap = dalloc<uint32_t>(g, c, c->v_hi - c->v_lo + 1, "exchange snapshot");
+        if (g->world > 1 && P.exchange) {
+            // sparse pays only below V*4 / (8 * world) pairs per rank: size for that
+            c->xcap = V / (2 * (uint64_t)g->world) + 1;
+            c->xsend = dalloc<uint2>(g, c, c->xcap, "exchange pairs (own)");
+            c->xrecv = dalloc<uint2>(g, c, c->xcap * g->world, "exchange pairs (all ranks)");
+            c->xcnt = dalloc<unsigned long long>(g, c, 1, "exchange pair count");
+            if (algo != ALGO_PR) c->snapfull = dalloc<uint32_t>(g, c, V, "exchange snapshot (full)");
+        }
         // ---- vertex state (the paper assumes it fits) ----
         if (algo == ALGO_PR) {
             c->rank = dalloc<float>(g, c, V, "rank");
@@ -801,6 +815,8 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                     pb, main);
         launch_fill(s, c->bounds_d, c->items, c->item_lo, c->item_hi, pb, c->q, main);
         timed_end(c, main, ep);
+        if (c->snapfull)   // values at iteration start, for the sparse exchange's change list
+            HYT_CUDA(cudaMemcpyAsync(c->snapfull, c->val, g->V * 4, cudaMemcpyDeviceToDevice, main));
         g->launches += (algo == ALGO_PR) ? 3 : 2;
         HYT_CUDA(cudaMemcpyAsync(c->parts_h + c->p_lo, c->parts_d + c->p_lo, np * sizeof(PartIter),
                                  cudaMemcpyDeviceToHost, main));
@@ -977,18 +993,49 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             HYT_CUDA(cudaStreamWaitEvent(main, c->ev_done[i], 0));
         }
         HYT_CUDA(cudaGetLastError());
-        // ---- multi-GPU exchange of pushed values (SURVEY §8e) ----
+        // ---- multi-GPU exchange of pushed values (SURVEY §8e, §8f #3) ----
         if (g->world > 1) {
-            if (algo == ALGO_PR) {
-                // own entries: residual + every rank's pushes; others: outbox -> zero again
-                dist_allreduce_sum_f32(g, c->delta, g->V, main);
+            const bool pr = algo == ALGO_PR;
+            bool sparse = false;
+            uint64_t maxc = 0;
+            if (c->xcap) {   // the pairs each rank changed; the largest count decides
+                HYT_CUDA(cudaMemsetAsync(c->xcnt, 0, 8, main));
+                launch_collect_changed(pr, g->V, c->v_lo, c->v_hi, c->val, c->snapfull, c->delta, c->xsend, c->xcap,
+                                       c->xcnt, main);
+                HYT_CUDA(cudaMemcpyAsync(c->red + 1, c->xcnt, 8, cudaMemcpyDeviceToDevice, main));
+                dist_allreduce_max_u64(g, c->red + 1, 1, main);
+                HYT_CUDA(cudaMemcpyAsync(&maxc, c->red + 1, 8, cudaMemcpyDeviceToHost, main));
+                HYT_CUDA(cudaStreamSynchronize(main));
+                g->launches += 1;
+                sparse = maxc <= c->xcap && (P.exchange == 2 || (uint64_t)g->world * maxc * 8 < g->V * 4);
+            }
+            if (sparse) {
+                if (maxc) {
+                    launch_pad_pairs(c->xsend, c->xcnt, maxc, main);
+                    dist_allgather_u32(g, (const uint32_t *)c->xsend, (uint32_t *)c->xrecv, 2 * maxc, main);
+                    launch_apply_pairs(pr, c->xrecv, (uint64_t)g->world * maxc, c->v_lo, c->v_hi, c->val, c->delta,
+                                       s.bm_next, main);
+                    g->launches += 2;
+                }
+                g->stats.exch_sparse += 1;
+                g->stats.exch_bytes += maxc * 8;
+            } else {
+                if (pr) {
+                    // own entries: residual + every rank's pushes; others: outbox -> zero again
+                    dist_allreduce_sum_f32(g, c->delta, g->V, main);
+                } else {
+                    HYT_CUDA(cudaMemcpyAsync(c->snap, c->val + c->v_lo, (c->v_hi - c->v_lo) * 4,
+                                             cudaMemcpyDeviceToDevice, main));
+                    dist_allreduce_min_u32(g, c->val, g->V, main);
+                    launch_mark_improved(c->val, c->snap, c->v_lo, c->v_hi, s.bm_next, main);
+                    g->launches += 1;
+                }
+                g->stats.exch_dense += 1;
+                g->stats.exch_bytes += g->V * 4;
+            }
+            if (pr) {   // the outbox is empty again
                 if (c->v_lo) HYT_CUDA(cudaMemsetAsync(c->delta, 0, c->v_lo * 4, main));
                 if (c->v_hi < g->V) HYT_CUDA(cudaMemsetAsync(c->delta + c->v_hi, 0, (g->V - c->v_hi) * 4, main));
-            } else {
-                HYT_CUDA(cudaMemcpyAsync(c->snap, c->val + c->v_lo, (c->v_hi - c->v_lo) * 4,
-                                         cudaMemcpyDeviceToDevice, main));
-                dist_allreduce_min_u32(g, c->val, g->V, main);
-                launch_mark_improved(c->val, c->snap, c->v_lo, c->v_hi, s.bm_next, main);
             }
         }
         // ---- next frontier ----

@@ -171,6 +171,12 @@ void launch_init_values(const DevState &s, uint64_t src_internal, const uint32_t
 // times a zero-copy probe over the mapped edge store (mode 0 random lines, 1 stream)
 float time_zc_probe(const uint4 *mapped, uint64_t nlines, int mode, uint32_t *sink, uint64_t *lines_read,
                     cudaStream_t st);
+void launch_collect_changed(int pr, uint64_t V, uint64_t lo, uint64_t hi, const uint32_t *val, const uint32_t *snap,
+                            const float *delta, uint2 *pairs, uint64_t cap, unsigned long long *cnt,
+                            cudaStream_t st);
+void launch_pad_pairs(uint2 *pairs, const unsigned long long *cnt, uint64_t n, cudaStream_t st);
+void launch_apply_pairs(int pr, const uint2 *pairs, uint64_t n, uint64_t lo, uint64_t hi, uint32_t *val,
+                        float *delta, uint32_t *bm_next, cudaStream_t st);
 void launch_mark_improved(const uint32_t *val, const uint32_t *snap, uint64_t lo, uint64_t hi, uint32_t *bm,
                           cudaStream_t st);
 void launch_gather_out(const DevState &s, const uint32_t *new_id, void *out_dev, cudaStream_t st);

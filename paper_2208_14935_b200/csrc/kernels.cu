@@ -406,6 +406,97 @@ void launch_mark_improved(const uint32_t *val, const uint32_t *snap, uint64_t lo
     k_mark_improved<<<(unsigned)blocks, 256, 0, st>>>(val, snap, lo, hi, bm);
 }
 
+// ---------------------------------------------------------------------------
+// Sparse inter-GPU exchange: (id, payload) pairs of the entries a
+// rank changed this iteration, all-gathered instead of a dense V-entry reduction.
+//   min-algorithms: every v with val[v] < its value at iteration start
+//   PR: every non-owned v with a non-zero delta (the outbox)
+// Each CTA appends its pairs through one atomicAdd; entries past `cap` are
+// counted but not written (the host then takes the dense path).
+// ---------------------------------------------------------------------------
+__global__ void k_collect_changed(int pr, uint64_t V, uint64_t lo, uint64_t hi, const uint32_t *__restrict__ val,
+                                  const uint32_t *__restrict__ snap, const float *__restrict__ delta,
+                                  uint2 *__restrict__ pairs, uint64_t cap, unsigned long long *cnt) {
+    __shared__ unsigned long long s_base;
+    __shared__ uint32_t s_n;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v0 = (uint64_t)blockIdx.x * blockDim.x; v0 < V; v0 += stride) {
+        const uint64_t v = v0 + threadIdx.x;
+        bool take = false;
+        uint32_t x = 0;
+        if (v < V) {
+            if (pr) {
+                const float d = delta[v];
+                take = (v < lo || v >= hi) && d != 0.0f;
+                x = __float_as_uint(d);
+            } else {
+                x = val[v];
+                take = x < snap[v];
+            }
+        }
+        if (threadIdx.x == 0) s_n = 0;
+        __syncthreads();
+        const uint32_t b = __ballot_sync(FULL_MASK, take);
+        uint32_t wbase = 0;
+        if ((threadIdx.x & 31) == 0 && b) wbase = atomicAdd(&s_n, (uint32_t)__popc(b));
+        wbase = __shfl_sync(FULL_MASK, wbase, 0);
+        __syncthreads();
+        if (threadIdx.x == 0) s_base = s_n ? atomicAdd(cnt, (unsigned long long)s_n) : 0ull;
+        __syncthreads();
+        if (take) {
+            const uint64_t k = s_base + wbase + __popc(b & ((1u << (threadIdx.x & 31)) - 1u));
+            if (k < cap) pairs[k] = make_uint2((uint32_t)v, x);
+        }
+        __syncthreads();
+    }
+}
+
+// fill [count, n) with the empty pair (id 0xFFFFFFFF) before the all-gather
+__global__ void k_pad_pairs(uint2 *pairs, const unsigned long long *cnt, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = *cnt + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride)
+        pairs[k] = make_uint2(0xFFFFFFFFu, 0u);
+}
+
+// apply every rank's pairs: min into val (and mark owned vertices another rank
+// lowered), or add the deltas addressed to this rank's vertices
+__global__ void k_apply_pairs(int pr, const uint2 *__restrict__ pairs, uint64_t n, uint64_t lo, uint64_t hi,
+                              uint32_t *val, float *delta, uint32_t *bm_next) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride) {
+        const uint2 p = pairs[k];
+        if (p.x == 0xFFFFFFFFu) continue;
+        const bool own = p.x >= lo && p.x < hi;
+        if (pr) {
+            if (own) atomicAdd(&delta[p.x], __uint_as_float(p.y));
+        } else {
+            const uint32_t old = atomicMin(&val[p.x], p.y);
+            if (own && p.y < old) atomicOr(&bm_next[p.x >> 5], 1u << (p.x & 31));
+        }
+    }
+}
+
+void launch_collect_changed(int pr, uint64_t V, uint64_t lo, uint64_t hi, const uint32_t *val, const uint32_t *snap,
+                            const float *delta, uint2 *pairs, uint64_t cap, unsigned long long *cnt,
+                            cudaStream_t st) {
+    uint64_t blocks = (V + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks == 0) blocks = 1;
+    k_collect_changed<<<(unsigned)blocks, 256, 0, st>>>(pr, V, lo, hi, val, snap, delta, pairs, cap, cnt);
+}
+
+void launch_pad_pairs(uint2 *pairs, const unsigned long long *cnt, uint64_t n, cudaStream_t st) {
+    k_pad_pairs<<<148, 256, 0, st>>>(pairs, cnt, n);
+}
+
+void launch_apply_pairs(int pr, const uint2 *pairs, uint64_t n, uint64_t lo, uint64_t hi, uint32_t *val,
+                        float *delta, uint32_t *bm_next, cudaStream_t st) {
+    uint64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks == 0) return;
+    k_apply_pairs<<<(unsigned)blocks, 256, 0, st>>>(pr, pairs, n, lo, hi, val, delta, bm_next);
+}
+
 // out[caller id] = value[new_id[caller id]]
 __global__ void k_gather_out(const uint32_t *__restrict__ vals, const uint32_t *__restrict__ new_id,
                              uint32_t *__restrict__ out, uint64_t V) {

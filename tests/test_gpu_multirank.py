@@ -95,3 +95,22 @@ def test_multirank_budget_and_cache(hyt, algo):
     outs = run_ranks(hyt, g, algo, 2, part=4096, edge_cache=1, edge_cache_bytes=g.E * d1 // 4)
     check(gkey, algo, outs)
     assert sum(st["parts_resident"] for _, st in outs) > 0
+
+
+@pytest.mark.parametrize("exchange", [0, 1, 2])
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+@pytest.mark.parametrize("engine", ["hybrid", "zerocopy"])
+def test_multirank_exchange_modes(hyt, exchange, world, algo, engine):
+    """the dense V-entry all-reduce (0), the per-iteration choice (1)
+    and the sparse pair all-gather whenever it fits (2) give the oracle's results."""
+    gkey = ("rmat", 9)
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    outs = run_ranks(hyt, g, algo, world, engine=engine, exchange=exchange)
+    check(gkey, algo, outs)
+    for _, st in outs:
+        assert st["exch_sparse"] + st["exch_dense"] == st["iterations"]
+        if exchange == 0:
+            assert st["exch_sparse"] == 0
+        if exchange == 2:
+            assert st["exch_sparse"] > 0
