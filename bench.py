@@ -22,6 +22,7 @@ values once per iteration.  Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import subprocess
@@ -391,6 +392,16 @@ def main():
     tags = hyt.TAGS
     kernel_tags = [1, 2, 3, 4, 5]          # relax: filter, compaction, zero-copy, resident, recompute
 
+    traffic_ratio, traffic_src = {}, None
+    tr_files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles",
+                                             "r*_relax_traffic.json")))
+    if tr_files:
+        try:
+            traffic_ratio = json.load(open(tr_files[-1]))["ratio"]
+            traffic_src = "profiles/" + os.path.basename(tr_files[-1])
+        except (OSError, ValueError, KeyError):
+            traffic_ratio = {}
+
     def tag_roof(i):
         if eng_launch[i] == 0:
             return None
@@ -408,6 +419,12 @@ def main():
                   "share_of_kernel_time": float(eng_ms[i] / max(1e-9, eng_ms[kernel_tags].sum()))})
         r["frac"] = r["achieved"] / r["peak"]
         r["traffic"] = None
+        kind = {1: "filter", 5: "filter", 4: "resident"}.get(i)
+        if kind and kind in traffic_ratio:
+            # DRAM bytes per algorithmic byte of this launch kind, from the committed
+            # ncu capture (tools/traffic_run.py), scaled to this run's average launch
+            r["traffic"] = traffic_ratio[kind] * alg
+            r["traffic_source"] = f"{traffic_src} (dram/alg = {traffic_ratio[kind]:.3f}, {kind} launches)"
         return r
 
     dom = max(kernel_tags, key=lambda i: eng_ms[i])

@@ -19,7 +19,7 @@ sys.path.insert(0, ROOT)
 
 
 DEFAULTS = {"relax_hot": 1, "relax_minb": 4, "relax_ctas_per_sm": 4, "zc_ctas_per_sm": 2, "edge_cache": 0,
-            "cost_model": 1, "recompute": 1, "priority": -1, "streams": 4}
+            "cost_model": 1, "recompute": 1, "priority": -1, "streams": 4, "k": 4, "exchange": 1}
 
 
 def main():
