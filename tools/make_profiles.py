@@ -76,7 +76,8 @@ def main():
     cfg_lines = ["# Full-size configurations (tools/run_configs.py, warm runs, O(E) certificates where run)\n",
                  "| config | V | E | budget GB | algo | mode | ms (runs) | iterations | transfer/edge | F/C/Z/R partitions | certificate |",
                  "|---|---:|---:|---:|---|---|---|---:|---:|---|---|"]
-    for name in ("cfg_fr.json", "cfg_fr_cal.json", "cfg_uk.json", "cfg_uk_cal.json"):
+    for name in ("cfg_fr.json", "cfg_fr_cal.json", "cfg_uk.json", "cfg_uk_cal.json", "cfg_r30s3.json",
+                 "cfg_r30s3_cal.json"):
         path = os.path.join(G, name)
         if not os.path.exists(path):
             continue
@@ -85,7 +86,8 @@ def main():
             cert = row.get("certificate", "")
             if isinstance(cert, dict):
                 cert = f"res_l1 {cert['res_l1']:.1f}, max rel res {cert['max_rel_res']:.1e}"
-            cfg_lines.append(f"| {d['config']} | {d['V']} | {d['E']} | {d['budget_gb']} | {row['algo']} | {row['mode']} | "
+            name_s = d['config'] + (f">>{d['shift']}" if d.get('shift') else "")
+            cfg_lines.append(f"| {name_s} | {d['V']} | {d['E']} | {d['budget_gb']} | {row['algo']} | {row['mode']} | "
                              f"{', '.join(f'{x:.1f}' for x in row['ms'])} | {row['iterations']} | "
                              f"{row['transfer_over_edge_volume']:.2f} | {'/'.join(str(x) for x in row['parts'])} | {cert} |")
     open(os.path.join(P, f"{r}_configs_full_size.md"), "w").write("\n".join(cfg_lines) + "\n")
