@@ -55,6 +55,9 @@ extern "C" {
 
 /* ---- load flags ---- */
 #define HYT_NO_HUBSORT 1u /* keep the caller's vertex order (skip P:452-462)        */
+#define HYT_SYMMETRIC  2u /* the caller asserts the edge set is symmetric (every    */
+                          /* (u,v) has (v,u), e.g. a symmetrised undirected graph): */
+                          /* enables pull iterations for BFS / CC (param direction) */
 
 /* ---- engine modes (hyt_set_param "engine_mode") ---- */
 #define HYT_MODE_HYBRID     0  /* the paper: per-partition cost-model selection    */
@@ -63,6 +66,10 @@ extern "C" {
 #define HYT_MODE_ZEROCOPY   3  /* every active partition -> ImpTM-zero-copy        */
 #define HYT_MODE_RESIDENT   4  /* edges copied once into device memory (build     */
                                /* extension); needs budget >= edges     */
+#define HYT_MODE_UM         5  /* ImpTM-UM comparison mode (Table V):   */
+                               /* edges in cudaMallocManaged memory advised         */
+                               /* ReadMostly, migrated on demand by the driver; the */
+                               /* budget is enforced by a device-memory balloon     */
 
 /* ---- engine ids in plans (hyt_debug_plan) ---- */
 #define HYT_ENG_NONE 0
@@ -108,6 +115,9 @@ typedef struct {
      * sparse pair all-gather / the dense V-entry reduction, and the payload
      * bytes each rank contributed (pairs x 8 B, or V x 4 B). */
     uint64_t exch_sparse, exch_dense, exch_bytes;
+    /* SEP-Graph switching: iterations run as pull; ImpTM-UM:   */
+    /* device bytes withheld from the driver so managed pages fit the budget     */
+    uint64_t pull_iters, um_balloon_bytes;
 } hyt_stats;
 
 /* One row per iteration (hyt_get_iter_log), the Fig. 7 / Table VI analog. */
@@ -115,7 +125,8 @@ typedef struct {
     uint64_t iteration;
     uint64_t active_vertices, active_edges;
     uint32_t parts_f, parts_c, parts_z, parts_r;
-    uint32_t units_f, pad;
+    uint32_t units_f;
+    uint32_t dir;                  /* 0 push (data-driven), 1 pull (topology-driven) */
     uint64_t bytes_f, bytes_c, bytes_z;
     double   ms;                   /* wall time of the iteration                  */
 } hyt_iter;
@@ -186,6 +197,18 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   changed when their bytes (world x max pairs x 8) are below the dense
  *   payload (V x 4), else dense; 2 sparse whenever the pairs fit the buffer.
  *   Results are the same either way.
+ *   direction [1] (BFS/CC on a graph loaded with HYT_SYMMETRIC
+ *   whose own partitions are all device-resident, one rank): 0 push only;
+ *   1 switch per iteration -- BFS by Beamer's rule (pull when frontier edges x
+ *   pull_alpha [14] > unexplored edges, back to push when frontier vertices x
+ *   pull_beta [24] < V), CC pull when frontier edges x cc_pull_alpha [2] > E;
+ *   2 pull in every iteration.  pull_heavy [1024]: lists longer than this are
+ *   split into slices across warps.  Results are identical either way.
+ *   um_balloon [1] (HYT_MODE_UM with a budget): 1 allocates the device memory
+ *   the budget leaves unused by others during the run so the driver keeps at
+ *   most the budget's remainder of managed pages resident; um_cold [1]: 1
+ *   evicts the managed pages to the host before every run (no reuse across
+ *   runs, like the paper's per-run measurements).
  * Errors: HYT_EINVAL on an unknown key or out-of-range value. */
 int hyt_set_param(hyt_graph *g, const char *key, double value);
 

@@ -31,7 +31,8 @@ HYT_OK, HYT_EINVAL, HYT_ENOMEM, HYT_ECUDA, HYT_ESTATE, HYT_ENCCL = 0, -1, -2, -3
 HYT_BFS, HYT_SSSP, HYT_CC, HYT_PR = 0, 1, 2, 3
 ALGOS = {"bfs": HYT_BFS, "sssp": HYT_SSSP, "cc": HYT_CC, "pr": HYT_PR}
 HYT_NO_HUBSORT = 1
-MODES = {"hybrid": 0, "filter": 1, "compaction": 2, "zerocopy": 3, "resident": 4}
+HYT_SYMMETRIC = 2
+MODES = {"hybrid": 0, "filter": 1, "compaction": 2, "zerocopy": 3, "resident": 4, "um": 5}
 HYT_ENG_NONE, HYT_ENG_F, HYT_ENG_C, HYT_ENG_Z, HYT_ENG_R = 0, 1, 2, 3, 4
 TAGS = ["plan", "filter", "compaction", "zerocopy", "resident", "recompute", "copy", "recompute_queue"]
 INF32 = 0xFFFFFFFF
@@ -47,14 +48,14 @@ class hyt_stats(ctypes.Structure):
         ("eng_launches", ctypes.c_uint64 * 8), ("eng_chunks", ctypes.c_uint64 * 8), ("eng_edges", ctypes.c_uint64 * 8),
         ("cal_link_gbs", ctypes.c_double), ("cal_cpt_gbs", ctypes.c_double), ("cal_zc_req_ns", ctypes.c_double),
         ("cal_zc_line_ns", ctypes.c_double), ("exch_sparse", ctypes.c_uint64), ("exch_dense", ctypes.c_uint64),
-        ("exch_bytes", ctypes.c_uint64)]
+        ("exch_bytes", ctypes.c_uint64), ("pull_iters", ctypes.c_uint64), ("um_balloon_bytes", ctypes.c_uint64)]
 
 
 class hyt_iter(ctypes.Structure):
     _fields_ = [("iteration", ctypes.c_uint64), ("active_vertices", ctypes.c_uint64),
                 ("active_edges", ctypes.c_uint64), ("parts_f", ctypes.c_uint32), ("parts_c", ctypes.c_uint32),
                 ("parts_z", ctypes.c_uint32), ("parts_r", ctypes.c_uint32), ("units_f", ctypes.c_uint32),
-                ("pad", ctypes.c_uint32), ("bytes_f", ctypes.c_uint64), ("bytes_c", ctypes.c_uint64),
+                ("dir", ctypes.c_uint32), ("bytes_f", ctypes.c_uint64), ("bytes_c", ctypes.c_uint64),
                 ("bytes_z", ctypes.c_uint64), ("ms", ctypes.c_double)]
 
 
@@ -151,7 +152,7 @@ class Graph:
         """Join an in-process group (one thread per rank; testing the multi-rank path on one GPU)."""
         check(hyt_init_dist_local(self.h, rank, world, group), "hyt_init_dist_local")
 
-    def load(self, off, nbr, w=None, hubsort: bool = True) -> None:
+    def load(self, off, nbr, w=None, hubsort: bool = True, symmetric: bool = False) -> None:
         off = np.ascontiguousarray(off, dtype=np.uint64)
         nbr = np.ascontiguousarray(nbr, dtype=np.uint32)
         if w is not None:
@@ -159,7 +160,8 @@ class Graph:
         V = len(off) - 1
         E = int(off[-1]) if V >= 0 else 0
         check(hyt_load_csr(self.h, V, E, _ptr(off), _ptr(nbr) if E else None, _ptr(w) if w is not None else None,
-                           0 if hubsort else HYT_NO_HUBSORT), "hyt_load_csr")
+                           (0 if hubsort else HYT_NO_HUBSORT) | (HYT_SYMMETRIC if symmetric else 0)),
+              "hyt_load_csr")
         self.V = V
 
     def run(self, algo, source: int = 0) -> None:
@@ -190,7 +192,7 @@ class Graph:
         check(hyt_get_iter_log(self.h, None, 0, ctypes.byref(n)), "hyt_get_iter_log")
         rows = (hyt_iter * max(1, n.value))()
         check(hyt_get_iter_log(self.h, ctypes.cast(rows, _vp), n.value, ctypes.byref(n)), "hyt_get_iter_log")
-        return [{f: getattr(rows[i], f) for f, _ in hyt_iter._fields_ if f != "pad"} for i in range(n.value)]
+        return [{f: getattr(rows[i], f) for f, _ in hyt_iter._fields_} for i in range(n.value)]
 
     def perm(self) -> np.ndarray:
         out = np.empty(self.V, dtype=np.uint32)

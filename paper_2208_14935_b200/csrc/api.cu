@@ -72,7 +72,7 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, cons
                  const uint32_t *w, uint32_t flags) {
     HYT_GUARD({
         HYT_REQUIRE(g, HYT_EINVAL, "null handle");
-        HYT_REQUIRE((flags & ~HYT_NO_HUBSORT) == 0, HYT_EINVAL, "unknown flags");
+        HYT_REQUIRE((flags & ~(HYT_NO_HUBSORT | HYT_SYMMETRIC)) == 0, HYT_EINVAL, "unknown flags");
         load_graph(g, V, E, off, nbr, w, flags);
     })
 }
@@ -96,7 +96,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "partition_bytes") { integral(); in(16, 1e12); p.partition_bytes = (uint64_t)v; }
         else if (k == "hub_fraction") { in(0, 1); HYT_REQUIRE(!g->loaded, HYT_ESTATE, "hub_fraction applies at load"); p.hub_fraction = v; }
         else if (k == "streams") { integral(); in(1, 8); p.streams = (int)v; }
-        else if (k == "engine_mode") { integral(); in(0, 4); p.engine_mode = (int)v; }
+        else if (k == "engine_mode") { integral(); in(0, 5); p.engine_mode = (int)v; }
         else if (k == "priority") { integral(); in(-1, 2); p.priority = (int)v; }
         else if (k == "recompute") { integral(); in(0, 1); p.recompute = (int)v; }
         else if (k == "damping") { in(1e-6, 1 - 1e-6); p.damping = v; }
@@ -118,6 +118,13 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "zc_line_ns") { in(0, 1e6); p.zc_line_ns = v; g->est_zc_line_ns = v; }
         else if (k == "thpt_cpt_gbs") { in(0, 1e6); p.thpt_cpt_gbs = v; g->est_cpt_gbs = v; }
         else if (k == "link_gbs") { in(0, 1e6); p.link_gbs = v; g->est_link_gbs = v; }
+        else if (k == "direction") { integral(); in(0, 2); p.direction = (int)v; }
+        else if (k == "pull_alpha") { in(1e-3, 1e9); p.pull_alpha = v; }
+        else if (k == "pull_beta") { in(1e-3, 1e9); p.pull_beta = v; }
+        else if (k == "cc_pull_alpha") { in(1e-3, 1e9); p.cc_pull_alpha = v; }
+        else if (k == "pull_heavy") { integral(); in(32, 1 << 30); p.pull_heavy = (uint64_t)v; }
+        else if (k == "um_balloon") { integral(); in(0, 1); p.um_balloon = (int)v; }
+        else if (k == "um_cold") { integral(); in(0, 1); p.um_cold = (int)v; }
         else throw Err{HYT_EINVAL, "unknown parameter '" + k + "'"};
         if (g->loaded) release_run_ctx(g);   // buffers depend on the parameters
     })

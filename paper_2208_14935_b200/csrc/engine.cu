@@ -272,6 +272,11 @@ struct RunCtx {
     uint32_t *outbuf = nullptr;   // u32[V] result staging for hyt_get_values
     uint4 *cache = nullptr;       // resident edge cache: chunks [cache_c0, ...) of partitions [p_lo, cache_hi)
     uint64_t cache_c0 = 0, cache_hi = 0, cache_bytes = 0;
+    uint4 *um = nullptr;          // ImpTM-UM: managed edge copy (cache points here)
+    // pull iterations (§8f #4): slices of the lists longer than pull_heavy
+    uint32_t *hs_v = nullptr;
+    uint64_t *hs_e0 = nullptr, *hs_e1 = nullptr;
+    uint64_t n_hs = 0;
     uint64_t v_lo = 0, v_hi = 0;  // own vertex range
     std::vector<void *> dev;      // arena blocks (released with the context)
     std::vector<void *> pinned;   // cudaHostAlloc blocks
@@ -293,6 +298,7 @@ static void destroy_ctx(hyt_graph *g, RunCtx *c) {
     for (auto e : c->ev_cbuf) if (e) cudaEventDestroy(e);
     for (auto it = c->dev.rbegin(); it != c->dev.rend(); ++it) g->arena.release(*it);
     for (auto p : c->pinned) pinned_free(p);
+    if (c->um) cudaFree(c->um);
     delete c->pool;
     delete c;
 }
@@ -356,6 +362,57 @@ static void fill_cache(hyt_graph *g, RunCtx *c, uint64_t p_hi_cache) {
     c->cache_c0 = c0;
     c->cache_hi = p_hi_cache;
     c->cache_bytes = (c1 - c0) * 16;
+}
+
+// ImpTM-UM comparison engine: the own partitions' edges
+// in managed memory advised ReadMostly, so the driver migrates (read-duplicates)
+// pages on first touch and evicts them under pressure.  Served as engine R: the
+// relax kernel dereferences the managed pointer directly.
+static void fill_um(hyt_graph *g, RunCtx *c) {
+    const uint64_t c0 = chunk_lo(g->off_h[c->bounds[c->p_lo]], c->d1);
+    const uint64_t c1 = chunk_hi(g->off_h[c->bounds[c->p_hi]], c->d1);
+    const uint64_t bytes = (c1 - c0 + 1) * 16;
+    HYT_CUDA(cudaMallocManaged((void **)&c->um, bytes, cudaMemAttachGlobal));
+    const char *src = reinterpret_cast<const char *>(host_edges(g, c->d1) + c0);
+    char *dst = reinterpret_cast<char *>(c->um);
+    const uint64_t n = (c1 - c0) * 16;
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned i = 0; i < nt; ++i)
+        th.emplace_back([=]() {
+            const uint64_t a = n * i / nt, b = n * (i + 1) / nt;
+            if (b > a) std::memcpy(dst + a, src + a, b - a);
+        });
+    for (auto &t : th) t.join();
+    HYT_CUDA(cudaMemAdvise(c->um, bytes, cudaMemAdviseSetReadMostly, g->device));
+    c->cache = c->um;
+    c->cache_c0 = c0;
+    c->cache_hi = c->p_hi;
+    c->cache_bytes = n;
+}
+
+// Slices of the long lists for pull iterations (one warp per slice).
+static void build_pull_slices(hyt_graph *g, RunCtx *c) {
+    const uint64_t H = g->prm.pull_heavy, S = 4096;
+    std::vector<uint32_t> sv;
+    std::vector<uint64_t> e0, e1;
+    for (uint64_t v = c->v_lo; v < c->v_hi; ++v) {
+        const uint64_t a = g->off_h[v], b = g->off_h[v + 1];
+        if (b - a <= H) continue;
+        for (uint64_t x = a; x < b; x += S) {
+            sv.push_back((uint32_t)v);
+            e0.push_back(x);
+            e1.push_back(std::min(b, x + S));
+        }
+    }
+    c->n_hs = sv.size();
+    if (!c->n_hs) return;
+    c->hs_v = dalloc<uint32_t>(g, c, c->n_hs, "pull slice vertices");
+    c->hs_e0 = dalloc<uint64_t>(g, c, c->n_hs, "pull slice begin");
+    c->hs_e1 = dalloc<uint64_t>(g, c, c->n_hs, "pull slice end");
+    HYT_CUDA(cudaMemcpy(c->hs_v, sv.data(), c->n_hs * 4, cudaMemcpyHostToDevice));
+    HYT_CUDA(cudaMemcpy(c->hs_e0, e0.data(), c->n_hs * 8, cudaMemcpyHostToDevice));
+    HYT_CUDA(cudaMemcpy(c->hs_e1, e1.data(), c->n_hs * 8, cudaMemcpyHostToDevice));
 }
 
 static RunCtx *build_ctx(hyt_graph *g, int algo) {
@@ -462,6 +519,8 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         if (P.engine_mode == MODE_RESIDENT) {
             // every own partition's edges once into device memory
             fill_cache(g, c, c->p_hi);
+        } else if (P.engine_mode == MODE_UM) {
+            fill_um(g, c);
         } else {
             const uint64_t rq_bytes_per_v = 28 + 4 + (algo == ALGO_PR ? 8 : 0);
             (void)rq_bytes_per_v;
@@ -537,6 +596,9 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 if (j > c->p_lo) fill_cache(g, c, j);
             }
         }
+        if (P.direction && g->symmetric && g->world == 1 && (algo == ALGO_BFS || algo == ALGO_CC) && c->cache &&
+            c->cache_hi == c->p_hi)
+            build_pull_slices(g, c);
         // streams
         const int nst = std::max(c->S, 1) + 2;
         while ((int)g->st.size() < nst) {
@@ -782,6 +844,35 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     for (int i = 0; i < ENG_COUNT; ++i) g->eng_chunks[i] = g->eng_edges[i] = 0;
     g->has_result = false;
 
+    // ImpTM-UM: cold pages, and a balloon so managed pages fit the budget's remainder
+    struct Balloon {
+        void *p = nullptr;
+        ~Balloon() { if (p) cudaFree(p); }
+    } balloon;
+    if (mode == MODE_UM && c->um) {
+        if (P.um_cold) {   // ReadMostly keeps duplicates on a prefetch: drop the hint, migrate, re-advise
+            HYT_CUDA(cudaMemAdvise(c->um, c->cache_bytes, cudaMemAdviseUnsetReadMostly, g->device));
+            HYT_CUDA(cudaMemPrefetchAsync(c->um, c->cache_bytes, cudaCpuDeviceId, main));
+            HYT_CUDA(cudaStreamSynchronize(main));
+            HYT_CUDA(cudaMemAdvise(c->um, c->cache_bytes, cudaMemAdviseSetReadMostly, g->device));
+        }
+        if (P.um_balloon && g->arena.budget) {
+            size_t fr = 0, tot = 0;
+            HYT_CUDA(cudaMemGetInfo(&fr, &tot));
+            const uint64_t room = g->arena.avail();
+            if (fr > room + (2ull << 20)) {
+                const uint64_t b = (fr - room) & ~((2ull << 20) - 1);
+                HYT_CUDA(cudaMalloc(&balloon.p, b));
+                g->stats.um_balloon_bytes = b;
+            }
+        }
+    }
+    const bool pull_ok = P.direction && g->symmetric && g->world == 1 && (algo == ALGO_BFS || algo == ALGO_CC) &&
+                         c->cache && c->cache_hi == c->p_hi && c->d1 == 4;
+    const uint64_t E_own = g->off_h[c->v_hi] - g->off_h[c->v_lo], V_own = c->v_hi - c->v_lo;
+    bool pulling = false;
+    uint64_t explored = 0;
+
     // source in internal ids
     uint64_t src_int = 0;
     if (algo == ALGO_BFS || algo == ALGO_SSSP) {
@@ -835,6 +926,22 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             active = a2;
         }
         if (active == 0) break;
+
+        // ---- SEP-Graph direction switch (§8f #4) ----
+        bool pull = false;
+        if (pull_ok) {
+            const double mf = (double)H.active_edges, nf = (double)H.active_vertices;
+            if (algo == ALGO_BFS) {   // Beamer's rule
+                explored += H.active_edges;
+                const double mu = E_own > explored ? (double)(E_own - explored) : 0.0;
+                if (P.direction == 2) pulling = true;
+                else if (!pulling) pulling = mf * P.pull_alpha > mu;
+                else pulling = !(nf * P.pull_beta < (double)V_own);
+            } else {
+                pulling = P.direction == 2 || mf * P.cc_pull_alpha > (double)E_own;
+            }
+            pull = pulling;
+        }
 
         hyt_iter row{};
         row.iteration = it;
@@ -925,8 +1032,21 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             g->launches += 1;
             g->eng_chunks[ENG_Z] += H.chunk_total[ENG_Z];
         }
+        // ---- pull iteration: topology-driven over the own range (§8f #4) ----
+        if (pull) {
+            EvPair e1;
+            timed_begin(c, main, e1, TAG_R);
+            const uint32_t *nbr = reinterpret_cast<const uint32_t *>(c->cache) - c->cache_c0 * 4;
+            launch_pull(algo, g->off_d, nbr, c->val, s.bm_cur, s.bm_next, c->v_lo, c->v_hi,
+                        (uint32_t)std::min<uint64_t>(P.pull_heavy, 0xFFFFFFFFu), c->hs_v, c->hs_e0, c->hs_e1, c->n_hs,
+                        main);
+            timed_end(c, main, e1);
+            g->launches += c->n_hs ? 2 : 1;
+            g->stats.pull_iters += 1;
+            row.dir = 1;
+        }
         // ---- resident (build extension) ----
-        if (H.ent_count[ENG_R]) {
+        if (H.ent_count[ENG_R] && !pull) {
             HYT_REQUIRE(c->cache != nullptr, HYT_ESTATE, "resident edges missing");
             cudaStream_t stm = g->st[0];
             EvPair e1;

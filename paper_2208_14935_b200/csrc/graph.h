@@ -80,6 +80,10 @@ struct Params {
     int cost_model = 1;        // 1: Eq. 1-3 with costs calibrated on this box; 0: the paper's PCIe-3 constants
     double zc_req_ns = 0;      // zero-copy random 128-B request time (0 = measure)
     double zc_line_ns = 0;     // zero-copy streamed 128-B line time (0 = measure)
+    int direction = 1;         // BFS/CC on symmetric resident graphs: 0 push, 1 switch (§8f #4), 2 pull
+    double pull_alpha = 14, pull_beta = 24, cc_pull_alpha = 2;
+    uint64_t pull_heavy = 1024;
+    int um_balloon = 1, um_cold = 1;   // ImpTM-UM comparison mode
 };
 
 CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio = 0.0, double zr_rtt = 0.0,
@@ -107,6 +111,7 @@ struct hyt_graph {
     bool loaded = false;
     uint64_t V = 0, E = 0;
     bool weighted = false;
+    bool symmetric = false;         // HYT_SYMMETRIC: enables pull iterations
     // Edge store: pinned mapped records of this rank's vertex range only
     // [store_v_lo, store_v_hi) (the whole graph when world == 1), starting at the
     // 16-byte chunk store_c0[0] (u32 ids) / store_c0[1] (id | w<<32) of the global

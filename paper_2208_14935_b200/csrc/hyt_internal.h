@@ -27,7 +27,7 @@ constexpr uint32_t kInf = 0xFFFFFFFFu;
 
 enum Algo : int { ALGO_BFS = 0, ALGO_SSSP = 1, ALGO_CC = 2, ALGO_PR = 3 };
 enum Eng : int { ENG_NONE = 0, ENG_F = 1, ENG_C = 2, ENG_Z = 3, ENG_R = 4, ENG_COUNT = 5 };
-enum Mode : int { MODE_HYBRID = 0, MODE_FILTER = 1, MODE_COMPACTION = 2, MODE_ZEROCOPY = 3, MODE_RESIDENT = 4 };
+enum Mode : int { MODE_HYBRID = 0, MODE_FILTER = 1, MODE_COMPACTION = 2, MODE_ZEROCOPY = 3, MODE_RESIDENT = 4, MODE_UM = 5 };
 
 __host__ __device__ inline uint64_t chunk_lo(uint64_t edge, uint32_t d1) { return (edge * d1) >> 4; }
 __host__ __device__ inline uint64_t chunk_hi(uint64_t edge, uint32_t d1) { return (edge * d1 + 15) >> 4; }
@@ -180,6 +180,12 @@ void launch_apply_pairs(int pr, const uint2 *pairs, uint64_t n, uint64_t lo, uin
 void launch_mark_improved(const uint32_t *val, const uint32_t *snap, uint64_t lo, uint64_t hi, uint32_t *bm,
                           cudaStream_t st);
 void launch_gather_out(const DevState &s, const uint32_t *new_id, void *out_dev, cudaStream_t st);
+
+// pull iteration over own vertices [v_lo, v_hi) with device-resident edges (pull.cu);
+// slices (sv, e0, e1) cover the lists longer than `heavy`
+void launch_pull(int algo, const uint64_t *off, const uint32_t *nbr, uint32_t *val, const uint32_t *bm_cur,
+                 uint32_t *bm_next, uint64_t v_lo, uint64_t v_hi, uint32_t heavy, const uint32_t *sv,
+                 const uint64_t *e0, const uint64_t *e1, uint64_t ns, cudaStream_t st);
 
 // ---- load-time kernels (load.cu) ----
 struct LoadOut;

@@ -330,7 +330,7 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
     HYT_CUDA(cudaSetDevice(g->device));
     Arena &A = g->arena;
     cudaStream_t st = g->main;
-    g->V = V; g->E = E; g->weighted = (w != nullptr);
+    g->V = V; g->E = E; g->weighted = (w != nullptr); g->symmetric = (flags & HYT_SYMMETRIC) != 0;
 
     // persistent device arrays
     g->off_d = arena_new<uint64_t>(A, V + 1, "offsets");
