@@ -268,7 +268,7 @@ def main():
 
     G = new_handle()
     t = time.time()
-    G.load(g.off, g.nbr, g.w)
+    G.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
     load_s = time.time() - t
 
     def barrier():
@@ -361,7 +361,7 @@ def main():
             s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s_ev.record(cur)
             H = new_handle()
-            H.load(g.off, g.nbr, g.w)
+            H.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
             step(H, out_bufs)
             e_ev.record(cur)
             barrier()
@@ -445,7 +445,9 @@ def main():
     per_algo = {}
     for a in algos:
         ms = float(np.mean(per_algo_ms[a]))
-        per_algo[a] = {"time_to_converge_s": ms / 1e3, "gteps": edges_per[a] / (ms / 1e3) / 1e9,
+        per_algo[a] = {"time_to_converge_s": ms / 1e3, "median_s": float(np.median(per_algo_ms[a])) / 1e3,
+                       "runs_s": [x / 1e3 for x in per_algo_ms[a]],
+                       "gteps": edges_per[a] / (ms / 1e3) / 1e9,
                        "edges": int(edges_per[a]), "iterations": int(iters[a])}
         if world > 1:
             per_algo[a]["exchange"] = exch[a]

@@ -184,3 +184,33 @@ def test_um_repeat_runs_and_warm(hyt):
             assert np.array_equal(G.values(), expected(key, "sssp"))
     finally:
         G.close()
+
+
+@pytest.fixture(scope="module")
+def fr_small():
+    return hytgen.make("fr", shift=3)          # FR-shaped recipe at 1/8 scale, symmetrised
+
+
+@pytest.mark.parametrize("algo", ["bfs", "cc"])
+def test_pull_fr_scale(hyt, fr_small, algo):
+    """FR-shaped graph at 1/8 scale (8.2M V, 451M stored edges), resident, push/pull
+    switching against the oracle, bit-exact, and pull must pay off."""
+    g = fr_small
+    want = oracle.bfs(g.off, g.nbr, 0) if algo == "bfs" else oracle.cc(g.off, g.nbr)
+    G = hyt.Graph(device=0)
+    try:
+        G.load(g.off, g.nbr, None, symmetric=True)
+        G.set("engine_mode", "resident")
+        ms = {}
+        for d in (0, 1):
+            G.set("direction", d)
+            G.run(algo, 0)
+            G.run(algo, 0)
+            st = G.stats()
+            assert np.array_equal(G.values(), want), d
+            assert (st["pull_iters"] > 0) == (d == 1)
+            ms[d] = st["time_ns"]
+    finally:
+        G.close()
+    if algo == "bfs":    # bottom-up steps skip most edges (measured 5.5x on the full FR shape)
+        assert ms[1] < ms[0], ms

@@ -43,7 +43,7 @@ def main():
     results = {"config": a.config, "shift": a.shift, "V": g.V, "E": g.E, "generate_s": gen_s, "rows": []}
     for b in [float(x) for x in a.budgets.split(",")]:
         G = hyt.Graph(device=0, budget=int(b * (1 << 30)))
-        G.load(g.off, g.nbr, g.w)
+        G.load(g.off, g.nbr, g.w, symmetric=bool(getattr(g, "symmetric", False)))
         for algo in a.algos.split(","):
             d1 = 8 if algo == "sssp" else 4
             edge_vol = g.E * d1
@@ -55,6 +55,7 @@ def main():
                     G.set("cost_model", 1 if "+cal" in mode else 0)
                     zw = [x for x in mode.split("+") if x.startswith("zw")]
                     G.set("zc_weight", float(zw[0][2:]) if zw else 1.0)
+                    G.set("direction", 2 if "+pullall" in mode else 1 if "+pull" in mode else 0)
                     G.set("engine_mode", mode.split("+")[0])
                     G.run(algo, 0)                 # warm-up (builds the run context)
                     vals = G.values()
@@ -75,6 +76,7 @@ def main():
                                 "link_gbs": link / (np.mean(ms) / 1e3) / 1e9,
                                 "parts_f": st["parts_filter"], "parts_c": st["parts_compaction"],
                                 "parts_z": st["parts_zerocopy"], "parts_r": st["parts_resident"],
+                                "pull_iters": st["pull_iters"], "um_balloon_bytes": st["um_balloon_bytes"],
                                 "eng_ms": dict(zip(hyt.TAGS, st["eng_ms"])),
                                 "device_bytes_peak": st["device_bytes_peak"],
                                 "calibration": [st["cal_link_gbs"], st["cal_cpt_gbs"], st["cal_zc_req_ns"],

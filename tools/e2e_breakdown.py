@@ -32,7 +32,7 @@ def main():
         G = hyt.Graph(device=0, budget=int(a.budget_gb * (1 << 30)))
         out[f"{rep}:handle_s"] = time.time() - t
         t = time.time()
-        G.load(g.off, g.nbr, g.w)
+        G.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
         out[f"{rep}:load_s"] = time.time() - t
         for algo in a.algos.split(","):
             for k in ("cold", "warm"):

@@ -34,7 +34,7 @@ def main():
     g = hytgen.make(a.config, shift=a.shift, weighted=True)
     print(f"generated {g.V} V {g.E} E in {time.time() - t:.1f}s", flush=True)
     G = hyt.Graph(device=0, budget=int(a.budget_gb * (1 << 30)))
-    G.load(g.off, g.nbr, g.w)
+    G.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
     G.set("engine_mode", a.engine)
     G.set("partition_bytes", a.part)
     for kv in a.set:

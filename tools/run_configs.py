@@ -40,7 +40,7 @@ def main():
     print(json.dumps({k: v for k, v in res.items() if k != "rows"}), flush=True)
     G = hyt.Graph(device=0, budget=int(a.budget_gb * (1 << 30)))
     t = time.time()
-    G.load(g.off, g.nbr, g.w)
+    G.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
     res["load_s"] = time.time() - t
     deg = np.diff(g.off.astype(np.int64))
     for mode in a.modes.split(","):
@@ -49,6 +49,7 @@ def main():
         G.set("cost_model", 1 if "+cal" in mode else 0)
         zw = [x for x in mode.split("+") if x.startswith("zw")]
         G.set("zc_weight", float(zw[0][2:]) if zw else 1.0)
+        G.set("direction", 2 if "+pullall" in mode else 1 if "+pull" in mode else 0)
         G.set("engine_mode", mode.split("+")[0])
         for algo in algos:
             G.run(algo, 0)                           # warm-up (run-context build, calibration)

@@ -44,7 +44,7 @@ def main():
     for engine in a.engines.split(","):
         budget = a.resident_budget_gb if engine == "resident" else a.budget_gb
         G = hyt.Graph(device=0, budget=int(budget * (1 << 30)))
-        G.load(g.off, g.nbr, g.w)
+        G.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
         for variant in a.variants.split(";"):
             G.set("engine_mode", engine)
             kvs = [kv.split("=") for kv in variant.split(",") if kv]

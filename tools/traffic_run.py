@@ -33,7 +33,7 @@ def run(a):
     import paper_2208_14935_b200 as hyt
     g = hytgen.make(a.config, shift=a.shift, weighted=True)
     G = hyt.Graph(device=0, budget=int(a.budget_gb * (1 << 30)))
-    G.load(g.off, g.nbr, g.w)
+    G.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
     G.set("engine_mode", a.engine)
     # one run (its context build and calibration launch no k_relax)
     tot_chunks = tot_edges = launches = 0
