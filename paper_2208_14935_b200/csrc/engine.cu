@@ -904,11 +904,12 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         const PlanBufs pb{c->parts_d, c->iagg, c->ibase, c->hdr_d};
         launch_plan(s, c->bounds_d, c->t_d, c->items, c->item_lo, c->item_hi, c->p_lo, c->p_hi, c->cache_hi, mode, cp,
                     pb, main);
-        launch_fill(s, c->bounds_d, c->items, c->item_lo, c->item_hi, pb, c->q, main);
+        // with pull possible, the queue is built only for push iterations (after the switch)
+        if (!pull_ok) launch_fill(s, c->bounds_d, c->items, c->item_lo, c->item_hi, pb, c->q, main);
         timed_end(c, main, ep);
         if (c->snapfull)   // values at iteration start, for the sparse exchange's change list
             HYT_CUDA(cudaMemcpyAsync(c->snapfull, c->val, g->V * 4, cudaMemcpyDeviceToDevice, main));
-        g->launches += (algo == ALGO_PR) ? 3 : 2;
+        g->launches += ((algo == ALGO_PR) ? 3 : 2) - (pull_ok ? 1 : 0);
         HYT_CUDA(cudaMemcpyAsync(c->parts_h + c->p_lo, c->parts_d + c->p_lo, np * sizeof(PartIter),
                                  cudaMemcpyDeviceToHost, main));
         HYT_CUDA(cudaMemcpyAsync(c->hdr_h, c->hdr_d, sizeof(SegHdr), cudaMemcpyDeviceToHost, main));
@@ -941,6 +942,14 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 pulling = P.direction == 2 || mf * P.cc_pull_alpha > (double)E_own;
             }
             pull = pulling;
+            if (!pull) {
+                EvPair ef;
+                timed_begin(c, main, ef, TAG_PLAN);
+                launch_fill(s, c->bounds_d, c->items, c->item_lo, c->item_hi, pb, c->q, main);
+                timed_end(c, main, ef);
+                g->launches += 1;
+                HYT_CUDA(cudaStreamWaitEvent(g->st[0], ef.b, 0));
+            }
         }
 
         hyt_iter row{};
