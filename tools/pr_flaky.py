@@ -1,0 +1,40 @@
+#!/usr/bin/env python
+"""Repeat the multi-rank PR parity case that failed once (world 3, compaction, rmat 4)
+and report the distribution of the error vs the oracle (signed and max)."""
+import json, os, sys
+import numpy as np
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
+import paper_2208_14935_b200 as hyt
+from test_gpu_parity import expected, gkey_graph
+from test_gpu_multirank import run_ranks
+
+
+def one(world, engine, gi, reps, **kw):
+    g = gkey_graph(("rmat", gi))
+    want = expected(("rmat", gi), "pr")
+    rows = []
+    for _ in range(reps):
+        if world == 1:
+            G = hyt.Graph(device=0)
+            G.load(g.off, g.nbr, g.w); G.set("engine_mode", engine); G.set("partition_bytes", 4096)
+            for k, v in kw.items():
+                G.set(k, v)
+            G.run("pr"); vals = G.values(); st = G.stats(); G.close()
+        else:
+            vals, st = run_ranks(hyt, g, "pr", world, engine=engine, **kw)[0]
+        rel = (vals.astype(np.float64) - want) / want
+        rows.append({"max_abs_rel": float(np.abs(rel).max()), "mean_rel": float(rel.mean()),
+                     "iters": st["iterations"], "sum_rank": float(vals.astype(np.float64).sum()),
+                     "sum_want": float(want.sum())})
+    return rows
+
+
+out = {}
+for world, engine, kw in [(3, "compaction", {}), (1, "compaction", {}), (3, "compaction", {"exchange": 0}),
+                          (2, "hybrid", {}), (1, "filter", {})]:
+    key = f"w{world}-{engine}-{kw}"
+    out[key] = one(world, engine, 4, 12, **kw)
+    m = [r["max_abs_rel"] for r in out[key]]
+    print(key, "max", max(m), "median", float(np.median(m)), "mean_rel", [round(r["mean_rel"], 7) for r in out[key]][:6], flush=True)
+json.dump(out, open("gpurun_out/pr_flaky.json", "w"), indent=1)
