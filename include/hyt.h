@@ -118,6 +118,7 @@ typedef struct {
     /* SEP-Graph switching: iterations run as pull; ImpTM-UM:   */
     /* device bytes withheld from the driver so managed pages fit the budget     */
     uint64_t pull_iters, um_balloon_bytes;
+    uint64_t exch_peer;            /* iterations exchanged by fused peer push (exchange = 3) */
 } hyt_stats;
 
 /* One row per iteration (hyt_get_iter_log), the Fig. 7 / Table VI analog. */
@@ -198,6 +199,12 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   all-reduce; 1 per iteration, all-gather the (id, value) pairs each rank
  *   changed when their bytes (world x max pairs x 8) are below the dense
  *   payload (V x 4), else dense; 2 sparse whenever the pairs fit the buffer.
+ *   3: fused peer push -- the relax kernels write a remote destination
+ *   straight into its owner's value / delta array and next-frontier bitmap
+ *   (atomicMin / atomicAdd / atomicOr through peer pointers: the same device
+ *   for an in-process group, CUDA IPC over NVLink for an NCCL job), so no
+ *   exchange collective follows the relax, only a barrier; one all-reduce of
+ *   the values at the end.  Needs <= 8 ranks and no caller arena.
  *   Results are the same either way.
  *   direction [1] (BFS/CC on a graph loaded with HYT_SYMMETRIC
  *   whose own partitions are all device-resident, one rank): 0 push only;

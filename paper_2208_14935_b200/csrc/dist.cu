@@ -144,6 +144,53 @@ static void local_allgather(hyt_graph *g, const void *send, void *recv, uint64_t
     local_barrier(G);
 }
 
+// ---------------------------------------------------------------------------
+// peer pointers for the fused push exchange (exchange = 3, §8e): every rank
+// publishes nptr device pointers; all[r * nptr + i] = rank r's pointer i, valid in
+// this process.  In-process group: the raw pointers (one device, or peers in one
+// process).  NCCL job: CUDA IPC handles of the cudaMalloc blocks, all-gathered,
+// then opened (lazy peer access over NVLink); dist_close_peers unmaps them.
+// ---------------------------------------------------------------------------
+void dist_share_ptrs(hyt_graph *g, void *const *mine, int nptr, void **all, std::vector<void *> &opened,
+                     cudaStream_t st) {
+    if (g->local_group) {
+        LocalGroup &G = *static_cast<LocalGroup *>(g->local_group);
+        HYT_CUDA(cudaStreamSynchronize(st));
+        G.slot[g->rank].assign((const uint8_t *)mine, (const uint8_t *)(mine + nptr));
+        local_barrier(G);
+        for (int r = 0; r < G.world; ++r) std::memcpy(all + r * nptr, G.slot[r].data(), nptr * sizeof(void *));
+        local_barrier(G);
+        return;
+    }
+    HYT_REQUIRE(g->nccl_comm, HYT_ESTATE, "peer exchange needs a multi-rank handle");
+    const uint64_t hb = sizeof(cudaIpcMemHandle_t);
+    std::vector<cudaIpcMemHandle_t> h(nptr);
+    for (int i = 0; i < nptr; ++i) HYT_CUDA(cudaIpcGetMemHandle(&h[i], mine[i]));
+    uint8_t *dsend = nullptr, *drecv = nullptr;
+    HYT_CUDA(cudaMalloc(&dsend, hb * nptr));
+    HYT_CUDA(cudaMalloc(&drecv, hb * nptr * g->world));
+    HYT_CUDA(cudaMemcpy(dsend, h.data(), hb * nptr, cudaMemcpyHostToDevice));
+    HYT_NCCL(nccl().AllGather(dsend, drecv, hb * nptr / 4, ncclUint32, g->nccl_comm, st));
+    std::vector<cudaIpcMemHandle_t> hall((size_t)nptr * g->world);
+    HYT_CUDA(cudaMemcpyAsync(hall.data(), drecv, hb * nptr * g->world, cudaMemcpyDeviceToHost, st));
+    HYT_CUDA(cudaStreamSynchronize(st));
+    cudaFree(dsend);
+    cudaFree(drecv);
+    for (int r = 0; r < g->world; ++r)
+        for (int i = 0; i < nptr; ++i) {
+            if (r == g->rank) { all[r * nptr + i] = mine[i]; continue; }
+            void *p = nullptr;
+            HYT_CUDA(cudaIpcOpenMemHandle(&p, hall[(size_t)r * nptr + i], cudaIpcMemLazyEnablePeerAccess));
+            opened.push_back(p);
+            all[r * nptr + i] = p;
+        }
+}
+
+void dist_close_peers(std::vector<void *> &opened) {
+    for (void *p : opened) cudaIpcCloseMemHandle(p);
+    opened.clear();
+}
+
 void dist_init_local(hyt_graph *g, int rank, int world, uint64_t group) {
     std::lock_guard<std::mutex> l(g_groups_mu);
     auto &sp = g_groups[group];

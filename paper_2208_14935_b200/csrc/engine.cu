@@ -272,6 +272,9 @@ struct RunCtx {
     uint32_t *outbuf = nullptr;   // u32[V] result staging for hyt_get_values
     uint4 *cache = nullptr;       // resident edge cache: chunks [cache_c0, ...) of partitions [p_lo, cache_hi)
     uint64_t cache_c0 = 0, cache_hi = 0, cache_bytes = 0;
+    // fused peer push (exchange = 3): every rank's (values | delta, bitmap a, bitmap b)
+    void *peer_ptr[kMaxPeers * 3] = {};
+    std::vector<void *> peer_opened;
     uint4 *um = nullptr;          // ImpTM-UM: managed edge copy (cache points here)
     // pull iterations (§8f #4): slices of the lists longer than pull_heavy
     uint32_t *hs_v = nullptr;
@@ -299,6 +302,7 @@ static void destroy_ctx(hyt_graph *g, RunCtx *c) {
     for (auto it = c->dev.rbegin(); it != c->dev.rend(); ++it) g->arena.release(*it);
     for (auto p : c->pinned) pinned_free(p);
     if (c->um) cudaFree(c->um);
+    dist_close_peers(c->peer_opened);
     delete c->pool;
     delete c;
 }
@@ -433,7 +437,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->outbuf = dalloc<uint32_t>(g, c, V, "result staging");
         if (g->world > 1 && algo != ALGO_PR)
             c->snap = dalloc<uint32_t>(g, c, c->v_hi - c->v_lo + 1, "exchange snapshot");
-        if (g->world > 1 && P.exchange) {
+        if (g->world > 1 && P.exchange && P.exchange != 3) {
             // sparse pays only below V*4 / (8 * world) pairs per rank: size for that
             c->xcap = V / (2 * (uint64_t)g->world) + 1;
             c->xsend = dalloc<uint2>(g, c, c->xcap, "exchange pairs (own)");
@@ -889,6 +893,36 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     HYT_CUDA(cudaMemsetAsync(c->racc, 0, 4 * sizeof(uint64_t), main));
     g->launches = 1;
 
+    // ---- fused peer push (exchange = 3): publish this rank's arrays, map the others' ----
+    const bool peer = g->world > 1 && P.exchange == 3;
+    PeerPush pp_it;
+    const PeerPush *ppp = nullptr;
+    struct PeerGuard {
+        RunCtx *c;
+        ~PeerGuard() { dist_close_peers(c->peer_opened); }
+    } peer_guard{c};
+    if (peer) {
+        HYT_REQUIRE(g->world <= kMaxPeers, HYT_EINVAL, "exchange = 3 supports at most 8 ranks");
+        HYT_REQUIRE(!g->arena.ext, HYT_EINVAL, "exchange = 3 needs library-allocated device memory (no arena)");
+        dist_close_peers(c->peer_opened);
+        void *mine[3] = {algo == ALGO_PR ? (void *)c->delta : (void *)c->val, (void *)c->bm_a, (void *)c->bm_b};
+        // also a barrier: every rank's values are initialised before anyone pushes into them
+        dist_share_ptrs(g, mine, 3, c->peer_ptr, c->peer_opened, main);
+        pp_it.n = (uint32_t)g->world;
+        pp_it.lo = c->v_lo;
+        pp_it.hi = c->v_hi;
+        for (int r = 0; r <= g->world; ++r) {
+            uint64_t lo = 0, hi = 0;
+            rank_vertex_range(g->off_h, g->world, std::min(r, g->world - 1), &lo, &hi);
+            pp_it.rb[r] = r < g->world ? lo : hi;
+        }
+        for (int r = 0; r < g->world; ++r) {
+            if (algo == ALGO_PR) pp_it.delta[r] = (float *)c->peer_ptr[3 * r];
+            else pp_it.val[r] = (uint32_t *)c->peer_ptr[3 * r];
+        }
+        ppp = &pp_it;
+    }
+
     const uint64_t np = c->p_hi - c->p_lo;
     std::vector<uint8_t> pvec(np);
     std::vector<uint64_t> units(2 * np + 2);
@@ -952,6 +986,9 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             }
         }
 
+        if (peer && algo != ALGO_PR)   // owners' next bitmaps: all ranks swap in lockstep
+            for (int r = 0; r < g->world; ++r) pp_it.bm[r] = (uint32_t *)c->peer_ptr[3 * r + ((it & 1) ? 1 : 2)];
+
         hyt_iter row{};
         row.iteration = it;
         row.active_vertices = H.active_vertices;
@@ -1009,7 +1046,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             }
             timed_begin(c, stm, e2, TAG_F);
             launch_relax(s, c->q, H.tile_base[ENG_F], fseg_first, fseg_end, H.chunk_total[ENG_F], c_lo, c_hi,
-                         nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot);
+                         nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot, ppp);
             timed_end(c, stm, e2);
             if (P.recompute) {   // process the loaded unit exactly once more
                 EvPair e4;
@@ -1017,7 +1054,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 launch_range_queue(s, v_lo, v_hi, c->rb[si], stm);
                 timed_end(c, stm, e4);
                 timed_begin(c, stm, e3, TAG_RECOMP);
-                launch_relax(s, c->rb[si].q, 0, 0, 0, 0, 0, 0, c->rb[si].total, es, relax_ctas, stm, P.relax_minb, P.relax_hot);
+                launch_relax(s, c->rb[si].q, 0, 0, 0, 0, 0, 0, c->rb[si].total, es, relax_ctas, stm, P.relax_minb, P.relax_hot, ppp);
                 timed_end(c, stm, e3);
             }
             g->launches += P.recompute ? 4 : 1;
@@ -1036,7 +1073,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 g->launches += 1;
             }
             launch_relax(s, c->q, H.tile_base[ENG_Z], H.ent_base[ENG_Z], H.ent_base[ENG_Z] + H.ent_count[ENG_Z],
-                         H.chunk_total[ENG_Z], 0, H.chunk_total[ENG_Z], nullptr, es, zc_ctas, stm, P.relax_minb, P.relax_hot);
+                         H.chunk_total[ENG_Z], 0, H.chunk_total[ENG_Z], nullptr, es, zc_ctas, stm, P.relax_minb, P.relax_hot, ppp);
             timed_end(c, stm, e1);
             g->launches += 1;
             g->eng_chunks[ENG_Z] += H.chunk_total[ENG_Z];
@@ -1066,7 +1103,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 g->launches += 1;
             }
             launch_relax(s, c->q, H.tile_base[ENG_R], H.ent_base[ENG_R], H.ent_base[ENG_R] + H.ent_count[ENG_R],
-                         H.chunk_total[ENG_R], 0, H.chunk_total[ENG_R], nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot);
+                         H.chunk_total[ENG_R], 0, H.chunk_total[ENG_R], nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot, ppp);
             timed_end(c, stm, e1);
             g->launches += 1;
             g->eng_chunks[ENG_R] += H.chunk_total[ENG_R];
@@ -1108,7 +1145,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 EdgeSrc es{c->cbuf[bi], 0, true};
                 timed_begin(c, stm, e2, TAG_C);
                 launch_relax(s, c->q, H.tile_base[ENG_C], H.ent_base[ENG_C], H.ent_base[ENG_C] + nC, total, w_lo,
-                             w_hi, nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot);
+                             w_hi, nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot, ppp);
                 timed_end(c, stm, e2);
                 g->launches += 1;
             }
@@ -1123,7 +1160,13 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         }
         HYT_CUDA(cudaGetLastError());
         // ---- multi-GPU exchange of pushed values ----
-        if (g->world > 1) {
+        if (peer) {
+            // fused push: remote relaxations already landed in their owners' arrays;
+            // a barrier keeps every rank's next plan after every rank's pushes
+            HYT_CUDA(cudaMemsetAsync(c->red + 1, 0, 8, main));
+            dist_allreduce_max_u64(g, c->red + 1, 1, main);
+            g->stats.exch_peer += 1;
+        } else if (g->world > 1) {
             const bool pr = algo == ALGO_PR;
             bool sparse = false;
             uint64_t maxc = 0;
@@ -1186,6 +1229,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         g->iter_log.push_back(row);
     }
     if (g->world > 1 && algo == ALGO_PR) dist_allreduce_sum_f32(g, c->rank, g->V, main);
+    if (peer && algo != ALGO_PR) dist_allreduce_min_u32(g, c->val, g->V, main);   // owners' values everywhere
     HYT_CUDA(cudaStreamSynchronize(main));
     harvest(g, c);
     const double t1 = now_ms();

@@ -68,7 +68,8 @@ struct Params {
     uint64_t compaction_buffer_bytes = 0;
     int zc_ctas_per_sm = 2;
     int relax_ctas_per_sm = 4;
-    int exchange = 1;          // multi-GPU: 0 dense, 1 sparse when cheaper (§8f #3), 2 sparse when it fits
+    int exchange = 1;          // multi-GPU: 0 dense, 1 sparse when cheaper (§8f #3), 2 sparse when it fits,
+                               // 3 fused peer push (relax writes remote destinations into their owner's memory)
     int relax_hot = 1;         // hub block in smem (PR Δ accumulation / min-algorithm value copy): 0 off, 1 auto, 2 always
     int relax_minb = 4;        // __launch_bounds__ min CTAs/SM of the relax kernel (4: 64 regs, 5: 51, 6: 42)
     int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
@@ -182,4 +183,7 @@ void dist_allreduce_sum_u64(hyt_graph *g, uint64_t *buf, uint64_t n, cudaStream_
 void dist_allreduce_max_u64(hyt_graph *g, uint64_t *buf, uint64_t n, cudaStream_t st);
 void dist_allgather_u32(hyt_graph *g, const uint32_t *send, uint32_t *recv, uint64_t n, cudaStream_t st);
 void dist_free(hyt_graph *g);
+void dist_share_ptrs(hyt_graph *g, void *const *mine, int nptr, void **all, std::vector<void *> &opened,
+                     cudaStream_t st);
+void dist_close_peers(std::vector<void *> &opened);
 }  // namespace hyt

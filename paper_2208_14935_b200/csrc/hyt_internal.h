@@ -111,6 +111,20 @@ struct DevState {
     float damping, epsilon;
 };
 
+// Fused multi-rank push (exchange = 3): a destination outside the own range
+// [rb[rank], rb[rank+1]) is relaxed straight into its owner's arrays through
+// these peer pointers (same device, or IPC-mapped over NVLink), so no exchange
+// collective follows the relax -- only a barrier.
+constexpr int kMaxPeers = 8;
+struct PeerPush {
+    uint32_t n = 0;                       // ranks (0 = off)
+    uint64_t lo = 0, hi = 0;              // own range
+    uint64_t rb[kMaxPeers + 1] = {};      // rank vertex bounds
+    uint32_t *val[kMaxPeers] = {};        // owners' value arrays (min-algorithms)
+    uint32_t *bm[kMaxPeers] = {};         // owners' NEXT frontier bitmaps (this iteration)
+    float *delta[kMaxPeers] = {};         // owners' delta arrays (PR)
+};
+
 struct QueueBufs {
     uint32_t *qv;        // entry -> vertex
     uint64_t *qpre;      // entry -> exclusive chunk prefix within its segment
@@ -164,7 +178,8 @@ struct EdgeSrc {
 // with seg_chunks chunks; dev_tot (range queues) overrides seg_end/seg_chunks/c_hi.
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
-                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb = 4, int hot = 1);
+                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb = 4, int hot = 1,
+                  const PeerPush *peer = nullptr);
 void launch_take_delta(const DevState &s, const QueueBufs &q, uint64_t e_lo, uint64_t e_hi, cudaStream_t st);
 void launch_range_queue(const DevState &s, uint64_t v_lo, uint64_t v_hi, RangeBufs r, cudaStream_t st);
 void launch_init_values(const DevState &s, uint64_t src_internal, const uint32_t *old_of, cudaStream_t st);

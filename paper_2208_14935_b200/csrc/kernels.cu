@@ -65,6 +65,7 @@ struct RelaxArgs {
     const uint4 *base;
     int64_t shift;
     uint32_t n_hot;            // hub-block size cached in shared memory (0 = off)
+    PeerPush pp;               // fused multi-rank push (PEER instantiations only)
 };
 
 constexpr int kWarps = kRelaxThreads / 32;
@@ -100,7 +101,18 @@ __device__ __forceinline__ void red_add_keep(float *p, float x, uint64_t pol) {
     asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(x), "l"(pol) : "memory");
 }
 
-template <int ALGO, bool COMPACT, int MINB>
+// owner rank of a remote destination (ranks own contiguous ranges)
+__device__ __forceinline__ int peer_owner(const PeerPush &pp, uint32_t d) {
+    int o = 0;
+#pragma unroll
+    for (int k = 1; k < kMaxPeers; ++k) o += (k < (int)pp.n && (uint64_t)d >= pp.rb[k]);
+    return o;
+}
+__device__ __forceinline__ bool peer_remote(const PeerPush &pp, uint32_t d) {
+    return (uint64_t)d < pp.lo || (uint64_t)d >= pp.hi;
+}
+
+template <int ALGO, bool COMPACT, int MINB, bool PEER>
 __global__ void __launch_bounds__(kRelaxThreads, MINB)
 k_relax(RelaxArgs A) {
     constexpr uint32_t D1 = (ALGO == ALGO_SSSP) ? 8u : 4u;
@@ -194,6 +206,7 @@ k_relax(RelaxArgs A) {
                         if (qd < lo || qd >= hi) continue;
                         const uint32_t dst = words[qd];
                         if (dst < n_hot) atomicAdd(&s_hot[dst], x);
+                        else if (PEER && peer_remote(A.pp, dst)) atomicAdd(&A.pp.delta[peer_owner(A.pp, dst)][dst], x);
                         else red_add_keep(&S.delta[dst], x, pol_keep);
                     }
                 }
@@ -247,7 +260,13 @@ k_relax(RelaxArgs A) {
                             const uint32_t d = dst[rr][qd], cn = cand[rr][qd];
                             if (cn < cur[rr][qd]) {
                                 if (d < n_hot && cn >= atomicMin(&s_hotw[d], cn)) continue;
-                                old[rr][qd] = atomicMin(&S.val[d], cn);
+                                if (PEER && peer_remote(A.pp, d)) {
+                                    // the owner's copy decides; the local copy only filters
+                                    old[rr][qd] = atomicMin(&A.pp.val[peer_owner(A.pp, d)][d], cn);
+                                    red_min_keep(&S.val[d], cn, pol_keep);
+                                } else {
+                                    old[rr][qd] = atomicMin(&S.val[d], cn);
+                                }
                             }
                         }
 #pragma unroll
@@ -255,7 +274,11 @@ k_relax(RelaxArgs A) {
 #pragma unroll
                         for (int qd = 0; qd < EPC; ++qd) {
                             const uint32_t d = dst[rr][qd];
-                            if (cand[rr][qd] < old[rr][qd]) atomicOr(&S.bm_next[d >> 5], 1u << (d & 31));
+                            if (cand[rr][qd] < old[rr][qd]) {
+                                uint32_t *bm = S.bm_next;
+                                if (PEER && peer_remote(A.pp, d)) bm = A.pp.bm[peer_owner(A.pp, d)];
+                                atomicOr(&bm[d >> 5], 1u << (d & 31));
+                            }
                         }
                 }
             }
@@ -266,19 +289,23 @@ k_relax(RelaxArgs A) {
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x) {
             const float x = s_hot[i];
-            if (x != 0.0f) atomicAdd(&S.delta[i], x);
+            if (x == 0.0f) continue;
+            if (PEER && peer_remote(A.pp, i)) atomicAdd(&A.pp.delta[peer_owner(A.pp, i)][i], x);
+            else atomicAdd(&S.delta[i], x);
         }
     }
 }
 
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
-                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb, int hot) {
+                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb, int hot,
+                  const PeerPush *peer) {
     RelaxArgs A;
     A.s = s; A.qv = q.qv; A.qpre = q.qpre; A.qbeg = q.qbeg; A.qdeg = q.qdeg; A.qaux = q.qaux;
     A.tile = q.tile + tile_base;
     A.c_lo = c_lo; A.c_hi = c_hi; A.seg_chunks = seg_chunks; A.seg_first = seg_first; A.seg_end = seg_end;
     A.dev_tot = dev_tot; A.base = src.base; A.shift = src.shift;
+    if (peer) A.pp = *peer;
     uint64_t grid;
     if (dev_tot) grid = (uint64_t)max_ctas;
     else {
@@ -296,11 +323,13 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     A.n_hot = 0;
     if (hot && s.algo == ALGO_PR) A.n_hot = (uint32_t)hv;
     else if (hot == 2 || (hot == 1 && !dev_tot && (c_hi - c_lo) >= grid * kWarps * 4 * kTile)) A.n_hot = (uint32_t)hv;
-#define HYT_RELAX_B(ALG, MB)                                                                     \
-    if (src.compact) k_relax<ALG, true, MB><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);      \
-    else k_relax<ALG, false, MB><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);
+#define HYT_RELAX_B(ALG, MB, PE)                                                                 \
+    if (src.compact) k_relax<ALG, true, MB, PE><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);  \
+    else k_relax<ALG, false, MB, PE><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);
 #define HYT_RELAX(ALG)                                                                           \
-    if (minb >= 6) { HYT_RELAX_B(ALG, 6) } else if (minb == 5) { HYT_RELAX_B(ALG, 5) } else { HYT_RELAX_B(ALG, 4) }
+    if (peer && peer->n) { HYT_RELAX_B(ALG, 4, true) }                                           \
+    else if (minb >= 6) { HYT_RELAX_B(ALG, 6, false) } else if (minb == 5) { HYT_RELAX_B(ALG, 5, false) } \
+    else { HYT_RELAX_B(ALG, 4, false) }
     switch (s.algo) {
         case ALGO_BFS: HYT_RELAX(ALGO_BFS); break;
         case ALGO_SSSP: HYT_RELAX(ALGO_SSSP); break;

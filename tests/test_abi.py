@@ -74,7 +74,7 @@ def test_binding_constants_match_header():
         assert defs[f"HYT_MODE_{name.upper()}"] == val, name
     for name in ("BFS", "SSSP", "CC", "PR"):
         assert defs[f"HYT_{name}"] == getattr(hyt, f"HYT_{name}")
-    # hyt_iter: 3 u64 + 6 u32 + 3 u64 + 1 double; hyt_stats ends with pull_iters, um_balloon_bytes
+    # hyt_iter: 3 u64 + 6 u32 + 3 u64 + 1 double; hyt_stats ends with pull_iters, um_balloon_bytes, exch_peer
     assert ctypes.sizeof(hyt.hyt_iter) == 3 * 8 + 6 * 4 + 3 * 8 + 8
-    assert [f for f, _ in hyt.hyt_stats._fields_][-2:] == ["pull_iters", "um_balloon_bytes"]
+    assert [f for f, _ in hyt.hyt_stats._fields_][-3:] == ["pull_iters", "um_balloon_bytes", "exch_peer"]
     assert "uint64_t pull_iters, um_balloon_bytes;" in txt and "uint32_t dir;" in txt

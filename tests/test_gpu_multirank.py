@@ -114,3 +114,71 @@ def test_multirank_exchange_modes(hyt, exchange, world, algo, engine):
             assert st["exch_sparse"] == 0
         if exchange == 2:
             assert st["exch_sparse"] > 0
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+@pytest.mark.parametrize("engine", ["hybrid", "filter", "compaction", "zerocopy", "resident"])
+@pytest.mark.parametrize("gi", [4, 9])
+def test_multirank_peer_push(hyt, world, algo, engine, gi):
+    """exchange = 3: the relax kernels write remote destinations straight into their
+    owners' arrays (fused push, no exchange collective); oracle's results."""
+    gkey = ("rmat", gi)
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    outs = run_ranks(hyt, g, algo, world, engine=engine, exchange=3)
+    check(gkey, algo, outs)
+    for _, st in outs:
+        assert st["exch_peer"] == st["iterations"] > 0
+        assert st["exch_sparse"] == st["exch_dense"] == 0
+
+
+@pytest.mark.parametrize("ci", range(len(CRAFTED)))
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "pr"])
+def test_multirank_peer_push_crafted(hyt, ci, algo):
+    gkey = ("crafted", ci)
+    g = gkey_graph(gkey)
+    outs = run_ranks(hyt, g, algo, 2, engine="hybrid", exchange=3)
+    check(gkey, algo, outs)
+
+
+def test_multirank_peer_push_repeat_runs(hyt):
+    """Several runs on the same handles: bitmaps swap parity across runs, pointers are
+    re-published, cached contexts are reused."""
+    gkey = ("rmat", 4)
+    g = gkey_graph(gkey)
+    seq = ["sssp", "pr", "bfs", "sssp", "bfs"]
+    world, key = 3, next(_group)
+    res, err = [[None] * len(seq) for _ in range(world)], [None] * world
+
+    def body(r):
+        G = None
+        try:
+            G = hyt.Graph(device=0)
+            G.init_dist_local(r, world, key)
+            G.load(g.off, g.nbr, g.w)
+            G.set("partition_bytes", 4096)
+            G.set("exchange", 3)
+            for j, algo in enumerate(seq):
+                G.run(algo, src_of(g) if algo in ("bfs", "sssp") else 0)
+                res[r][j] = G.values()
+        except Exception as e:          # noqa: BLE001
+            err[r] = e
+        finally:
+            if G is not None:
+                G.close()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    for e in err:
+        if e is not None:
+            raise e
+    for j, algo in enumerate(seq):
+        want = expected(gkey, algo)
+        for r in range(world):
+            if algo == "pr":
+                assert_pr_close(res[r][j], want)
+            else:
+                assert np.array_equal(res[r][j], want), (algo, j, r)
