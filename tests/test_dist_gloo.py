@@ -193,3 +193,88 @@ def test_rank_split_hub_larger_than_share():
     for a, b in zip(rs, rs[1:]):
         assert a["v_hi"] == b["v_lo"] and a["p_hi"] == b["p_lo"]
     assert any(x["v_hi"] == x["v_lo"] for x in rs)
+
+
+# --------------------------------------------------------------------------- exchange = 3
+# The fused peer push on CPU: shared-memory tensors stand in for the peer pointers
+# (rank r's value array and its two frontier bitmaps, which every rank can write),
+# a per-owner lock stands in for the atomics, and gloo gives the barrier after the
+# pushes, the termination sum and the final MIN all-reduce.  Bitmaps swap in
+# lockstep, so iteration parity picks the owner's "next" bitmap (csrc/engine.cu).
+
+def _peer_worker(rank, world, port, algo, shared, locks, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = _graph(symmetric=(algo == "cc"))
+        rr = [hyt.rank_range(g.off, 8 if algo == "sssp" else 4, 4096, world, r) for r in range(world)]
+        lo, hi = rr[rank]["v_lo"], rr[rank]["v_hi"]
+        owner = np.zeros(g.V, dtype=np.int64)
+        for r in range(world):
+            owner[rr[r]["v_lo"]:rr[r]["v_hi"]] = r
+        val = [shared[r][0].numpy() for r in range(world)]
+        bm = [[shared[r][1].numpy(), shared[r][2].numpy()] for r in range(world)]
+        mine = val[rank]
+        mine[:] = np.arange(g.V) if algo == "cc" else INF     # init own array (full length)
+        if algo != "cc" and lo <= 0 < hi:
+            mine[0] = 0
+        bm[rank][0][:] = False
+        bm[rank][1][:] = False
+        bm[rank][0][lo:hi] = True if algo == "cc" else (np.arange(lo, hi) == 0)
+        dist.barrier()                                          # publish: initialised before any push
+        it = 0
+        while True:
+            cur, nxt = bm[rank][it & 1], [bm[r][(it + 1) & 1] for r in range(world)]
+            n = torch.tensor([int(cur[lo:hi].sum())], dtype=torch.int64)
+            dist.all_reduce(n)
+            if n.item() == 0:
+                break
+            for u in np.nonzero(cur[lo:hi])[0] + lo:
+                for k in range(int(g.off[u]), int(g.off[u + 1])):
+                    v = int(g.nbr[k])
+                    cand = mine[u] + (1 if algo == "bfs" else int(g.w[k])) if algo != "cc" else mine[u]
+                    o = int(owner[v])
+                    with locks[o]:                              # atomicMin on the owner, then its bit
+                        if cand < val[o][v]:
+                            val[o][v] = cand
+                            nxt[o][v] = True
+                    if o != rank:
+                        mine[v] = min(mine[v], cand)            # local copy: a filter only
+            cur[lo:hi] = False                                  # owner clears its consumed bitmap
+            dist.barrier()                                      # every push has landed
+            it += 1
+        t = torch.from_numpy(mine.astype(np.int64).copy())
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)                # owners' values everywhere
+        q.put((rank, it, t.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc"])
+def test_gloo_peer_push_matches_oracle(algo):
+    world = 2
+    g = _graph(symmetric=(algo == "cc"))
+    shared = [(torch.zeros(g.V, dtype=torch.int64).share_memory_(),
+               torch.zeros(g.V, dtype=torch.bool).share_memory_(),
+               torch.zeros(g.V, dtype=torch.bool).share_memory_()) for _ in range(world)]
+    ctx = mp.get_context("spawn")
+    locks = [ctx.Lock() for _ in range(world)]
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_peer_worker, args=(r, world, port, algo, shared, locks, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if algo == "bfs":
+        want = oracle.bfs(g.off, g.nbr, 0)
+    elif algo == "sssp":
+        want = oracle.sssp(g.off, g.nbr, g.w, 0)
+    else:
+        want = oracle.cc(g.off, g.nbr)
+    for _, iters, vals in out:
+        assert iters > 0
+        assert np.array_equal(vals.astype(np.uint32), want)
