@@ -153,14 +153,14 @@ def measured_h2d_gbs(device: int) -> float:
 
 
 def pin_host(arrays) -> list:
-    """cudaHostRegister (portable | mapped) of host arrays; returns those registered."""
+    """cudaHostRegister (portable | mapped | read-only) of host arrays; returns those registered."""
     import torch
     cr = torch.cuda.cudart()
     done = []
     for a in arrays:
         if a is None or a.nbytes == 0:
             continue
-        rc = cr.cudaHostRegister(a.ctypes.data, a.nbytes, 3)
+        rc = cr.cudaHostRegister(a.ctypes.data, a.nbytes, 1 | 2 | 8)
         if rc == 0 or str(rc).endswith("success"):
             done.append(a)
     return done

@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <exception>
 #include <mutex>
 #include <sys/mman.h>
 #include <thread>
@@ -351,6 +352,32 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
     HYT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
 
     phase("validate + device alloc");
+    // One rank owns every edge, so the store's size is known now: pin it on a host
+    // thread while the GPU computes in-degrees and the hub sort.
+    struct EarlyStore {
+        std::thread th;
+        void *n = nullptr, *w = nullptr;
+        std::exception_ptr err;
+        ~EarlyStore() {
+            if (th.joinable()) th.join();
+            pinned_free(n);
+            pinned_free(w);
+        }
+    } early;
+    const uint64_t early_nbytes = ((E * 4 + 15) & ~15ull) + 32, early_wbytes = ((E * 8 + 15) & ~15ull) + 32;
+    if (g->world == 1) {
+        const int dev = g->device;
+        const bool weighted = w != nullptr;
+        early.th = std::thread([&early, dev, weighted, early_nbytes, early_wbytes] {
+            try {
+                cudaSetDevice(dev);
+                early.n = pinned_alloc(early_nbytes);
+                if (weighted) early.w = pinned_alloc(early_wbytes);
+            } catch (...) {
+                early.err = std::current_exception();
+            }
+        });
+    }
     HostView vn, vw;
     try {
         vn.open(nbr, E * 4);
@@ -442,10 +469,18 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         g->store_c0[1] = e_lo / 2;                          // first chunk of u64 records
         const uint64_t nbase = g->store_c0[0] * 4, wbase = g->store_c0[1] * 2;
         const uint64_t nbytes = (((e_hi - nbase) * 4 + 15) & ~15ull) + 32;
-        g->nbr_h = (uint32_t *)pinned_alloc(nbytes);      // zero-filled (padding included)
-        if (w) {
-            const uint64_t wbytes = (((e_hi - wbase) * 8 + 15) & ~15ull) + 32;
-            g->ew_h = (uint64_t *)pinned_alloc(wbytes);
+        const uint64_t wbytes = (((e_hi - wbase) * 8 + 15) & ~15ull) + 32;
+        if (early.th.joinable()) {
+            early.th.join();
+            if (early.err) std::rethrow_exception(early.err);
+            HYT_REQUIRE(nbytes == early_nbytes && (!w || wbytes == early_wbytes), HYT_ESTATE,
+                        "edge store size mismatch");
+            g->nbr_h = (uint32_t *)early.n;                 // ownership moves to the handle
+            g->ew_h = (uint64_t *)early.w;
+            early.n = early.w = nullptr;
+        } else {
+            g->nbr_h = (uint32_t *)pinned_alloc(nbytes);  // zero-filled (padding included)
+            if (w) g->ew_h = (uint64_t *)pinned_alloc(wbytes);
         }
         uint32_t *nbr_out = nullptr;
         uint64_t *ew_out = nullptr;

@@ -21,12 +21,18 @@ def main():
     ap.add_argument("--shift", type=int, default=0)
     ap.add_argument("--algos", default="sssp,pr")
     ap.add_argument("--budget-gb", type=float, default=16.0)
+    ap.add_argument("--pin", type=int, default=0, help="page-lock the caller arrays first (bench.py's e2e)")
     a = ap.parse_args()
     import numpy as np
     import hytgen
     import paper_2208_14935_b200 as hyt
     g = hytgen.make(a.config, shift=a.shift, weighted=True)
-    out = {}
+    out = {"pin": a.pin}
+    if a.pin:
+        from bench import pin_host
+        t = time.time()
+        out["pinned"] = len(pin_host([g.off, g.nbr, g.w]))
+        out["pin_s"] = time.time() - t
     for rep in range(2):
         t = time.time()
         G = hyt.Graph(device=0, budget=int(a.budget_gb * (1 << 30)))
