@@ -280,6 +280,7 @@ struct RunCtx {
     uint32_t *hs_v = nullptr;
     uint64_t *hs_e0 = nullptr, *hs_e1 = nullptr;
     uint64_t n_hs = 0;
+    uint32_t *bm_glob = nullptr;  // multi-rank pull BFS: every rank's frontier (OR of own words)
     uint64_t v_lo = 0, v_hi = 0;  // own vertex range
     std::vector<void *> dev;      // arena blocks (released with the context)
     std::vector<void *> pinned;   // cudaHostAlloc blocks
@@ -600,9 +601,11 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 if (j > c->p_lo) fill_cache(g, c, j);
             }
         }
-        if (P.direction && g->symmetric && g->world == 1 && (algo == ALGO_BFS || algo == ALGO_CC) && c->cache &&
-            c->cache_hi == c->p_hi)
+        if (P.direction && g->symmetric && (algo == ALGO_BFS || (algo == ALGO_CC && g->world == 1)) && c->cache &&
+            c->cache_hi == c->p_hi) {
             build_pull_slices(g, c);
+            if (g->world > 1) c->bm_glob = dalloc<uint32_t>(g, c, W + 2, "global frontier");
+        }
         // streams
         const int nst = std::max(c->S, 1) + 2;
         while ((int)g->st.size() < nst) {
@@ -871,9 +874,19 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             }
         }
     }
-    const bool pull_ok = P.direction && g->symmetric && g->world == 1 && (algo == ALGO_BFS || algo == ALGO_CC) &&
-                         c->cache && c->cache_hi == c->p_hi && c->d1 == 4;
-    const uint64_t E_own = g->off_h[c->v_hi] - g->off_h[c->v_lo], V_own = c->v_hi - c->v_lo;
+    bool pull_ok = P.direction && g->symmetric && (algo == ALGO_BFS || (algo == ALGO_CC && g->world == 1)) &&
+                   c->cache && c->cache_hi == c->p_hi && c->d1 == 4 && (g->world == 1 || c->bm_glob);
+    if (g->world > 1 && P.direction && g->symmetric && algo == ALGO_BFS) {
+        // every rank must take the same branch (the pull gathers the frontier): AND over ranks
+        uint32_t f = pull_ok ? 1u : 0u;
+        HYT_CUDA(cudaMemcpyAsync(c->red, &f, 4, cudaMemcpyHostToDevice, main));
+        dist_allreduce_min_u32(g, (uint32_t *)c->red, 1, main);
+        HYT_CUDA(cudaMemcpyAsync(&f, c->red, 4, cudaMemcpyDeviceToHost, main));
+        HYT_CUDA(cudaStreamSynchronize(main));
+        pull_ok = f != 0;
+    }
+    // the switch rule uses whole-graph quantities (all ranks decide alike)
+    const uint64_t E_own = g->E, V_own = g->V;
     bool pulling = false;
     uint64_t explored = 0;
 
@@ -951,23 +964,24 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         HYT_CUDA(cudaGetLastError());
         harvest(g, c);
         const SegHdr H = *c->hdr_h;
-        uint64_t active = H.active_vertices;
-        if (g->world > 1) {   // total active vertices over all ranks (termination)
-            HYT_CUDA(cudaMemcpyAsync(c->red, &c->hdr_d->active_vertices, 8, cudaMemcpyDeviceToDevice, main));
-            dist_allreduce_sum_u64(g, c->red, 1, main);
-            uint64_t a2 = 0;
-            HYT_CUDA(cudaMemcpyAsync(&a2, c->red, 8, cudaMemcpyDeviceToHost, main));
+        uint64_t active = H.active_vertices, active_e = H.active_edges;
+        if (g->world > 1) {   // total active vertices (termination) and edges (direction switch) over all ranks
+            HYT_CUDA(cudaMemcpyAsync(c->red, &c->hdr_d->active_vertices, 16, cudaMemcpyDeviceToDevice, main));
+            dist_allreduce_sum_u64(g, c->red, 2, main);
+            uint64_t a2[2] = {0, 0};
+            HYT_CUDA(cudaMemcpyAsync(a2, c->red, 16, cudaMemcpyDeviceToHost, main));
             HYT_CUDA(cudaStreamSynchronize(main));
-            active = a2;
+            active = a2[0];
+            active_e = a2[1];
         }
         if (active == 0) break;
 
         // ---- SEP-Graph direction switch (§8f #4) ----
         bool pull = false;
         if (pull_ok) {
-            const double mf = (double)H.active_edges, nf = (double)H.active_vertices;
+            const double mf = (double)active_e, nf = (double)active;
             if (algo == ALGO_BFS) {   // Beamer's rule
-                explored += H.active_edges;
+                explored += active_e;
                 const double mu = E_own > explored ? (double)(E_own - explored) : 0.0;
                 if (P.direction == 2) pulling = true;
                 else if (!pulling) pulling = mf * P.pull_alpha > mu;
@@ -1083,9 +1097,17 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             EvPair e1;
             timed_begin(c, main, e1, TAG_R);
             const uint32_t *nbr = reinterpret_cast<const uint32_t *>(c->cache) - c->cache_c0 * 4;
-            launch_pull(algo, g->off_d, nbr, c->val, s.bm_cur, s.bm_next, c->v_lo, c->v_hi,
+            const uint32_t *front = s.bm_cur;
+            if (g->world > 1) {   // OR of every rank's own frontier words (disjoint bits: a sum)
+                launch_own_words(s.bm_cur, c->bm_glob, s.W, c->v_lo, c->v_hi, main);
+                HYT_CUDA(cudaMemsetAsync(c->bm_glob + s.W, 0, 8, main));
+                dist_allreduce_sum_u64(g, reinterpret_cast<uint64_t *>(c->bm_glob), (s.W + 1) / 2, main);
+                front = c->bm_glob;
+                g->launches += 1;
+            }
+            launch_pull(algo, g->off_d, nbr, c->val, front, s.bm_next, c->v_lo, c->v_hi,
                         (uint32_t)std::min<uint64_t>(P.pull_heavy, 0xFFFFFFFFu), c->hs_v, c->hs_e0, c->hs_e1, c->n_hs,
-                        main);
+                        (uint32_t)(it + 1), main);
             timed_end(c, main, e1);
             g->launches += c->n_hs ? 2 : 1;
             g->stats.pull_iters += 1;

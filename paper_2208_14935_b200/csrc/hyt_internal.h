@@ -200,7 +200,8 @@ void launch_gather_out(const DevState &s, const uint32_t *new_id, void *out_dev,
 // slices (sv, e0, e1) cover the lists longer than `heavy`
 void launch_pull(int algo, const uint64_t *off, const uint32_t *nbr, uint32_t *val, const uint32_t *bm_cur,
                  uint32_t *bm_next, uint64_t v_lo, uint64_t v_hi, uint32_t heavy, const uint32_t *sv,
-                 const uint64_t *e0, const uint64_t *e1, uint64_t ns, cudaStream_t st);
+                 const uint64_t *e0, const uint64_t *e1, uint64_t ns, uint32_t lvl, cudaStream_t st);
+void launch_own_words(const uint32_t *bm, uint32_t *out, uint64_t nw, uint64_t lo, uint64_t hi, cudaStream_t st);
 
 // ---- load-time kernels (load.cu) ----
 struct LoadOut;

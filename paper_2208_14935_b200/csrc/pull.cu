@@ -6,10 +6,12 @@
 // (no queue), and a vertex reads the frontier bits of its neighbours instead of
 // frontier vertices writing into their neighbours.  On a symmetric graph the out-list
 // of v is also its in-list, so no transposed CSR is needed.
-//   BFS: an unvisited v takes level(u) + 1 from the FIRST neighbour u found in the
-//        frontier and stops scanning (Beamer's bottom-up step).  Exact only when the
-//        iteration is level-synchronous, which holds when every own partition is
-//        resident (no recompute pass, one rank): the engine enables pull only then.
+//   BFS: an unvisited v takes the iteration's level (frontier level + 1) once it finds
+//        ANY neighbour in the frontier and stops scanning (Beamer's bottom-up step).
+//        Exact only when iterations are level-synchronous, which holds when every
+//        own partition of every rank is resident (no recompute pass): the engine
+//        enables pull only then.  With several ranks the frontier read is the OR of
+//        every rank's own frontier words (one all-reduce per pull iteration).
 //   CC:  every v takes min(label(v), min over frontier neighbours label(u)).  Correct
 //        under any schedule: the push invariant "label(v) <= label(u) on every edge
 //        unless u is in the frontier" is kept because v pulls from every frontier u.
@@ -31,6 +33,7 @@ struct PullArgs {
     uint32_t *bm_next;
     uint64_t v_lo, v_hi;
     uint32_t heavy;            // lists longer than this go to the slice kernel
+    uint32_t lvl;              // BFS: level assigned by this (level-synchronous) iteration
 };
 
 __device__ __forceinline__ bool in_frontier(const uint32_t *bm, uint32_t u) {
@@ -64,8 +67,8 @@ __global__ void __launch_bounds__(256) k_pull(PullArgs A) {
             for (uint64_t j = 0; j < deg; ++j) {
                 const uint32_t u = __ldg(&A.nbr[beg + j]);
                 if (!in_frontier(A.bm_cur, u)) continue;
+                if (ALGO == ALGO_BFS) { best = A.lvl; break; }
                 const uint32_t x = __ldcg(&A.val[u]);
-                if (ALGO == ALGO_BFS) { best = x + 1u; break; }
                 best = x < best ? x : best;
             }
             if (best < cur) { A.val[v] = best; mark(A.bm_next, v); }
@@ -84,11 +87,10 @@ __global__ void __launch_bounds__(256) k_pull(PullArgs A) {
                 bool f = false;
                 if (j + lane < d) {
                     const uint32_t u = __ldg(&A.nbr[b + j + lane]);
-                    if (in_frontier(A.bm_cur, u)) { x = __ldcg(&A.val[u]); f = true; }
+                    if (in_frontier(A.bm_cur, u)) { x = ALGO == ALGO_BFS ? 0u : __ldcg(&A.val[u]); f = true; }
                 }
                 if (ALGO == ALGO_BFS) {
-                    const uint32_t hit = __ballot_sync(FULL_MASK, f);
-                    if (hit) { best = __shfl_sync(FULL_MASK, x, __ffs(hit) - 1) + 1u; break; }
+                    if (__ballot_sync(FULL_MASK, f)) { best = A.lvl; break; }
                 } else {
                     best = x < best ? x : best;
                 }
@@ -121,11 +123,10 @@ __global__ void __launch_bounds__(256) k_pull_heavy(PullArgs A, const uint32_t *
             bool f = false;
             if (j + lane < z) {
                 const uint32_t u = __ldg(&A.nbr[j + lane]);
-                if (in_frontier(A.bm_cur, u)) { x = __ldcg(&A.val[u]); f = true; }
+                if (in_frontier(A.bm_cur, u)) { x = ALGO == ALGO_BFS ? 0u : __ldcg(&A.val[u]); f = true; }
             }
             if (ALGO == ALGO_BFS) {
-                const uint32_t hit = __ballot_sync(FULL_MASK, f);
-                if (hit) { best = __shfl_sync(FULL_MASK, x, __ffs(hit) - 1) + 1u; break; }
+                if (__ballot_sync(FULL_MASK, f)) { best = A.lvl; break; }
             } else {
                 best = x < best ? x : best;
             }
@@ -142,10 +143,25 @@ __global__ void __launch_bounds__(256) k_pull_heavy(PullArgs A, const uint32_t *
     }
 }
 
+// out = the words of bm restricted to [lo, hi), zero elsewhere (nw words)
+__global__ void k_own_words(const uint32_t *__restrict__ bm, uint32_t *__restrict__ out, uint64_t nw, uint64_t lo,
+                            uint64_t hi) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw; w += stride)
+        out[w] = bm[w] & range_mask(w, lo, hi);
+}
+
+void launch_own_words(const uint32_t *bm, uint32_t *out, uint64_t nw, uint64_t lo, uint64_t hi, cudaStream_t st) {
+    uint64_t grid = (nw + 255) / 256;
+    if (grid > 148ull * 8) grid = 148ull * 8;
+    if (grid == 0) return;
+    k_own_words<<<(unsigned)grid, 256, 0, st>>>(bm, out, nw, lo, hi);
+}
+
 void launch_pull(int algo, const uint64_t *off, const uint32_t *nbr, uint32_t *val, const uint32_t *bm_cur,
                  uint32_t *bm_next, uint64_t v_lo, uint64_t v_hi, uint32_t heavy, const uint32_t *sv,
-                 const uint64_t *e0, const uint64_t *e1, uint64_t ns, cudaStream_t st) {
-    PullArgs A{off, nbr, val, bm_cur, bm_next, v_lo, v_hi, heavy};
+                 const uint64_t *e0, const uint64_t *e1, uint64_t ns, uint32_t lvl, cudaStream_t st) {
+    PullArgs A{off, nbr, val, bm_cur, bm_next, v_lo, v_hi, heavy, lvl};
     const uint64_t n = v_hi > v_lo ? v_hi - v_lo : 0;
     uint64_t grid = (n + 255) / 256;
     if (grid > 148ull * 8) grid = 148ull * 8;

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 _group = itertools.count(1000)
 
 
-def run_ranks(hyt, g, algo, world, engine="hybrid", part=4096, budget=0, **kw):
+def run_ranks(hyt, g, algo, world, engine="hybrid", part=4096, budget=0, symmetric=False, **kw):
     key = next(_group)
     out, err = [None] * world, [None] * world
 
@@ -27,7 +27,7 @@ def run_ranks(hyt, g, algo, world, engine="hybrid", part=4096, budget=0, **kw):
         try:
             G = hyt.Graph(device=0, budget=budget)
             G.init_dist_local(r, world, key)
-            G.load(g.off, g.nbr, g.w)
+            G.load(g.off, g.nbr, g.w, symmetric=symmetric)
             G.set("engine_mode", engine)
             G.set("partition_bytes", part)
             for k, v in kw.items():
@@ -182,3 +182,45 @@ def test_multirank_peer_push_repeat_runs(hyt):
                 assert_pr_close(res[r][j], want)
             else:
                 assert np.array_equal(res[r][j], want), (algo, j, r)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("direction", [1, 2])
+@pytest.mark.parametrize("exchange", [0, 1, 3])
+@pytest.mark.parametrize("gi", [3, 4, 8, 11])
+def test_multirank_pull_bfs(hyt, world, direction, exchange, gi):
+    """Pull (bottom-up) BFS across ranks: the frontier is the OR of every rank's own
+    words; levels stay bit-exact with every exchange mode."""
+    gkey = ("rmat", gi)
+    g = symmetric_version(gkey)
+    want = oracle_bfs_sym(gkey)
+    outs = run_ranks(hyt, g, "bfs", world, engine="resident", symmetric=True, direction=direction,
+                     exchange=exchange, pull_heavy=64)
+    for vals, st in outs:
+        assert np.array_equal(vals, want)
+        assert st["pull_iters"] > 0
+        if direction == 2:
+            assert st["pull_iters"] == st["iterations"]
+
+
+def test_multirank_pull_needs_every_rank_resident(hyt):
+    """An edge cache that holds every partition on some ranks only: no rank pulls."""
+    gkey = ("rmat", 7)
+    g = symmetric_version(gkey)
+    want = oracle_bfs_sym(gkey)
+    outs = run_ranks(hyt, g, "bfs", 2, engine="hybrid", symmetric=True, direction=2, edge_cache=1,
+                     edge_cache_bytes=int(g.off[g.V // 3]) * 4)
+    for vals, st in outs:
+        assert np.array_equal(vals, want)
+        assert st["pull_iters"] == 0
+
+
+_bfs_sym_cache = {}
+
+
+def oracle_bfs_sym(gkey):
+    if gkey not in _bfs_sym_cache:
+        import oracle
+        g = symmetric_version(gkey)
+        _bfs_sym_cache[gkey] = oracle.bfs(g.off, g.nbr, src_of(g))
+    return _bfs_sym_cache[gkey]
