@@ -118,8 +118,10 @@ def run_gpu(hyt, g, algo, engine="hybrid", part=32 << 20, prio="auto", budget=0,
 
 
 def assert_pr_close(got, want):
-    rel = np.abs(got.astype(np.float64) - want) / want
-    assert rel.max() <= PR_TOL, f"max rel err {rel.max():.3e} at {rel.argmax()}"
+    signed = (got.astype(np.float64) - want) / want
+    rel = np.abs(signed)
+    assert rel.max() <= PR_TOL, (f"max rel err {rel.max():.3e} at {rel.argmax()}; mean signed {signed.mean():.3e}, "
+                                 f"min signed {signed.min():.3e}, sum ratio {got.sum(dtype=np.float64) / want.sum():.8f}")
 
 
 ALL_KEYS = [("rmat", i) for i in range(len(RMATS))] + [("crafted", i) for i in range(len(CRAFTED))]
