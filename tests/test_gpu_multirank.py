@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 _group = itertools.count(1000)
 
 
-def run_ranks(hyt, g, algo, world, engine="hybrid", part=4096, budget=0, symmetric=False, **kw):
+def run_ranks(hyt, g, algo, world, engine="hybrid", part=4096, budget=0, symmetric=False, per_rank=None, **kw):
     key = next(_group)
     out, err = [None] * world, [None] * world
 
@@ -32,6 +32,8 @@ def run_ranks(hyt, g, algo, world, engine="hybrid", part=4096, budget=0, symmetr
             G.set("partition_bytes", part)
             for k, v in kw.items():
                 G.set(k, v)
+            for k, v in (per_rank or {}).items():
+                G.set(k, v[r])
             G.run(algo, src_of(g) if algo in ("bfs", "sssp") else 0)
             out[r] = (G.values(), G.stats())
         except Exception as e:          # noqa: BLE001 -- re-raised in the main thread
@@ -208,11 +210,18 @@ def test_multirank_pull_needs_every_rank_resident(hyt):
     gkey = ("rmat", 7)
     g = symmetric_version(gkey)
     want = oracle_bfs_sym(gkey)
+    # rank 0 caches everything it owns, rank 1 a quarter of its edges
     outs = run_ranks(hyt, g, "bfs", 2, engine="hybrid", symmetric=True, direction=2, edge_cache=1,
-                     edge_cache_bytes=int(g.off[g.V // 3]) * 4)
+                     per_rank={"edge_cache_bytes": [0, g.E * 4 // 8]})
     for vals, st in outs:
         assert np.array_equal(vals, want)
         assert st["pull_iters"] == 0
+    assert outs[0][1]["parts_resident"] > 0
+    # both cache everything: pull
+    outs = run_ranks(hyt, g, "bfs", 2, engine="hybrid", symmetric=True, direction=2, edge_cache=1)
+    for vals, st in outs:
+        assert np.array_equal(vals, want)
+        assert st["pull_iters"] == st["iterations"] > 0
 
 
 _bfs_sym_cache = {}
