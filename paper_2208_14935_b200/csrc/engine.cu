@@ -601,8 +601,10 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 if (j > c->p_lo) fill_cache(g, c, j);
             }
         }
-        if (P.direction && g->symmetric && (algo == ALGO_BFS || (algo == ALGO_CC && g->world == 1)) && c->cache &&
-            c->cache_hi == c->p_hi) {
+        // CC pulls neighbours' labels: across ranks only with an exchange that leaves
+        // every rank's copy current (dense / sparse), not with the peer push
+        const bool cc_pull = algo == ALGO_CC && (g->world == 1 || P.exchange != 3);
+        if (P.direction && g->symmetric && (algo == ALGO_BFS || cc_pull) && c->cache && c->cache_hi == c->p_hi) {
             build_pull_slices(g, c);
             if (g->world > 1) c->bm_glob = dalloc<uint32_t>(g, c, W + 2, "global frontier");
         }
@@ -874,9 +876,10 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             }
         }
     }
-    bool pull_ok = P.direction && g->symmetric && (algo == ALGO_BFS || (algo == ALGO_CC && g->world == 1)) &&
-                   c->cache && c->cache_hi == c->p_hi && c->d1 == 4 && (g->world == 1 || c->bm_glob);
-    if (g->world > 1 && P.direction && g->symmetric && algo == ALGO_BFS) {
+    const bool cc_pull = algo == ALGO_CC && (g->world == 1 || P.exchange != 3);
+    bool pull_ok = P.direction && g->symmetric && (algo == ALGO_BFS || cc_pull) && c->cache &&
+                   c->cache_hi == c->p_hi && c->d1 == 4 && (g->world == 1 || c->bm_glob);
+    if (g->world > 1 && P.direction && g->symmetric && (algo == ALGO_BFS || cc_pull)) {
         // every rank must take the same branch (the pull gathers the frontier): AND over ranks
         uint32_t f = pull_ok ? 1u : 0u;
         HYT_CUDA(cudaMemcpyAsync(c->red, &f, 4, cudaMemcpyHostToDevice, main));

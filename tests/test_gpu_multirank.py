@@ -205,6 +205,27 @@ def test_multirank_pull_bfs(hyt, world, direction, exchange, gi):
             assert st["pull_iters"] == st["iterations"]
 
 
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("direction", [1, 2])
+@pytest.mark.parametrize("exchange", [0, 1, 2, 3])
+@pytest.mark.parametrize("gi", [3, 4, 8])
+def test_multirank_pull_cc(hyt, world, direction, exchange, gi):
+    """Pull CC across ranks reads the neighbours' labels from the local full-length copy,
+    which the dense / sparse exchanges keep current; with the peer push (3) it stays push."""
+    gkey = ("rmat", gi)
+    g = symmetric_version(gkey)
+    outs = run_ranks(hyt, g, "cc", world, engine="resident", symmetric=True, direction=direction,
+                     exchange=exchange, pull_heavy=64)
+    check(gkey, "cc", outs)
+    for _, st in outs:
+        if exchange == 3:
+            assert st["pull_iters"] == 0
+        else:
+            assert st["pull_iters"] > 0
+            if direction == 2:
+                assert st["pull_iters"] == st["iterations"]
+
+
 def test_multirank_pull_needs_every_rank_resident(hyt):
     """An edge cache that holds every partition on some ranks only: no rank pulls."""
     gkey = ("rmat", 7)
