@@ -1,7 +1,7 @@
 # Builds the product library (sm_100a) and the CPU-side test infrastructure.
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr $(EXTRA)
 SRC_DIR := paper_2208_14935_b200/csrc
 LIB := paper_2208_14935_b200/lib/libhyt.so
 SRCS := $(SRC_DIR)/plan.cu $(SRC_DIR)/kernels.cu $(SRC_DIR)/load.cu $(SRC_DIR)/engine.cu $(SRC_DIR)/api.cu $(SRC_DIR)/dist.cu $(SRC_DIR)/pull.cu

@@ -154,8 +154,10 @@ int hyt_set_device_arena(hyt_graph *g, void *dptr, uint64_t bytes);
  *   nbr_host      : u32[E] neighbour ids (< V).
  *   w_host        : u32[E] edge weights (SSSP) or NULL.
  *   flags         : 0, or HYT_NO_HUBSORT and/or HYT_SYMMETRIC (the caller
- *                   asserts every (u,v) has (v,u); not checked, and a wrong
- *                   claim makes pull iterations wrong).
+ *                   asserts every (u,v) has (v,u).  The load checks the
+ *                   necessary condition in-degree = out-degree for every
+ *                   vertex (HYT_EINVAL otherwise); a claim that passes it but
+ *                   is still false makes pull iterations wrong).
  * The library hub-sorts (top ceil(0.08 V) by D_o*D_i first,
  * descending, ties by id; the rest in natural order), relabels on the GPU and
  * stores the edges in library-owned pinned, mapped host memory (ids u32[E];

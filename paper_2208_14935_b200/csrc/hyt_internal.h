@@ -19,7 +19,10 @@ constexpr int kChunkBytes = 16;
 constexpr int kRelaxThreads = 256;      // threads per relax CTA (8 independent warps)
 constexpr int kChunksPerThread = 4;     // 16-byte loads in flight per lane
 constexpr int kTile = 32 * kChunksPerThread;   // chunks per WARP tile (2 KiB of edges)
-constexpr int kHotV = 4096;             // PR: pushes to vertices < kHotV (the hub block) go to smem first
+#ifndef HYT_HOTV
+#define HYT_HOTV 4096
+#endif
+constexpr int kHotV = HYT_HOTV;         // PR: pushes to vertices < kHotV (the hub block) go to smem first
 constexpr int kItemWords = 256;         // bitmap words (8192 vertices) per plan item
 constexpr int kItemThreads = 256;       // threads per plan / fill / range CTA
 

@@ -76,6 +76,15 @@ __global__ void k_indeg(const uint32_t *__restrict__ nbr, uint64_t E, uint64_t V
     }
 }
 
+// HYT_SYMMETRIC sanity check: a symmetric edge multiset has D_i(v) = D_o(v) for
+// every v (necessary, not sufficient; it catches a directed graph declared symmetric).
+__global__ void k_sym_degrees(const uint64_t *__restrict__ off, const uint32_t *__restrict__ din, uint64_t V,
+                              uint32_t *__restrict__ bad) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride)
+        if ((uint64_t)din[v] != off[v + 1] - off[v]) *bad = 2;
+}
+
 // H(v) = D_o D_i / (D_omax D_imax): the denominator is common, so the exact
 // integer key D_o*D_i orders the vertices as H does.
 __device__ __forceinline__ uint64_t hub_key(const uint64_t *off, const uint32_t *din, uint64_t v) {
@@ -388,6 +397,12 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         HYT_CUDA(cudaMemcpyAsync(&bad_h, bad, 4, cudaMemcpyDeviceToHost, st));
         HYT_CUDA(cudaStreamSynchronize(st));
         HYT_REQUIRE(bad_h == 0, HYT_EINVAL, "neighbour id >= V");
+        if (flags & HYT_SYMMETRIC) {
+            k_sym_degrees<<<grid_for(V), 256, 0, st>>>(off_old, din, V, bad);
+            HYT_CUDA(cudaMemcpyAsync(&bad_h, bad, 4, cudaMemcpyDeviceToHost, st));
+            HYT_CUDA(cudaStreamSynchronize(st));
+            HYT_REQUIRE(bad_h == 0, HYT_EINVAL, "HYT_SYMMETRIC: some vertex's in-degree differs from its out-degree");
+        }
         phase("in-degrees (zero-copy)");
 
         // ---- hub sort: top h = ceil(frac*V) by D_o*D_i ----

@@ -214,3 +214,15 @@ def test_pull_fr_scale(hyt, fr_small, algo):
         G.close()
     if algo == "bfs":    # bottom-up steps skip most edges (measured 5.5x on the full FR shape)
         assert ms[1] < ms[0], ms
+
+
+def test_symmetric_flag_checked_at_load(hyt):
+    """A directed graph declared symmetric fails the in-degree = out-degree check."""
+    g = hytgen.rmat_csr(10, 1024, 8192, seed=77)          # directed
+    G = hyt.Graph(device=0)
+    try:
+        with pytest.raises(hyt.HytError) as ei:
+            G.load(g.off, g.nbr, symmetric=True)
+        assert ei.value.code == hyt.HYT_EINVAL and "HYT_SYMMETRIC" in str(ei.value)
+    finally:
+        G.close()
