@@ -57,6 +57,10 @@ def main():
                     G.set("zc_weight", float(zw[0][2:]) if zw else 1.0)
                     G.set("direction", 2 if "+pullall" in mode else 1 if "+pull" in mode else 0)
                     G.set("engine_mode", mode.split("+")[0])
+                    for tok in mode.split("+")[1:]:
+                        if "=" in tok:                 # "+key=value": any library parameter
+                            k, v = tok.split("=")
+                            G.set(k, float(v))
                     G.run(algo, 0)                 # warm-up (builds the run context)
                     vals = G.values()
                     edges = int(deg[vals != 0xFFFFFFFF].sum()) if algo in ("sssp", "bfs") else g.E
