@@ -666,6 +666,7 @@ static DevState make_state(hyt_graph *g, RunCtx *c) {
     s.d1 = c->d1; s.algo = c->algo;
     s.damping = (float)g->prm.damping;
     s.epsilon = (float)g->prm.epsilon;
+    s.hot_v = (uint32_t)g->prm.relax_hot_v;
     return s;
 }
 

@@ -112,6 +112,7 @@ struct DevState {
     uint32_t d1;
     int algo;
     float damping, epsilon;
+    uint32_t hot_v;             // hub-block size in shared memory (relax_hot_v)
 };
 
 // Fused multi-rank push (exchange = 3): a destination outside the own range

@@ -123,7 +123,7 @@ k_relax(RelaxArgs A) {
     __shared__ uint32_t s_deg[kWarps][kTile + 1];
     __shared__ uint32_t s_src[kWarps][kTile + 1];
     __shared__ uint32_t s_mask[kWarps][kChunksPerThread];
-    __shared__ uint32_t s_hotw[kHotV];            // PR: f32 Δ accumulators; else hub values
+    extern __shared__ uint32_t s_hotw[];          // hub block (dynamic, n_hot words): PR Δ accumulators; else hub values
     float *s_hot = reinterpret_cast<float *>(s_hotw);
     const DevState &S = A.s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -296,6 +296,29 @@ k_relax(RelaxArgs A) {
     }
 }
 
+// Launch with a dynamic hub block of `smem` bytes: raise the kernel's dynamic shared
+// memory limit once, and cap the persistent grid at what stays resident (a second
+// wave of a grid-stride kernel would double the tail).
+static void relax_go(void (*k)(RelaxArgs), const RelaxArgs &A, uint64_t grid, size_t smem, cudaStream_t st) {
+    struct Occ { void (*k)(RelaxArgs); size_t smem; int per_sm; };
+    static thread_local Occ cache[64];
+    static thread_local int ncache = 0;
+    int per_sm = -1;
+    for (int i = 0; i < ncache; ++i)
+        if (cache[i].k == k && cache[i].smem == smem) { per_sm = cache[i].per_sm; break; }
+    if (per_sm < 0) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kRelaxThreads, smem) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+        if (ncache < 64) cache[ncache++] = Occ{k, smem, per_sm};
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (grid > (uint64_t)sms * per_sm) grid = (uint64_t)sms * per_sm;
+    k<<<(unsigned)grid, kRelaxThreads, smem, st>>>(A);
+}
+
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
                   const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb, int hot,
@@ -319,13 +342,14 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     // only when every warp has >= 4 tiles (64 KiB of edges per CTA against the 16 KiB
     // hub-value load); range queues (device-side size) do not qualify.  hot = 2
     // forces it on (tests), 0 turns both off.
-    const uint64_t hv = s.V < (uint64_t)kHotV ? s.V : (uint64_t)kHotV;
+    const uint64_t hv = s.V < (uint64_t)s.hot_v ? s.V : (uint64_t)s.hot_v;
     A.n_hot = 0;
     if (hot && s.algo == ALGO_PR) A.n_hot = (uint32_t)hv;
     else if (hot == 2 || (hot == 1 && !dev_tot && (c_hi - c_lo) >= grid * kWarps * 4 * kTile)) A.n_hot = (uint32_t)hv;
+    const size_t smem = (size_t)A.n_hot * 4;
 #define HYT_RELAX_B(ALG, MB, PE)                                                                 \
-    if (src.compact) k_relax<ALG, true, MB, PE><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);  \
-    else k_relax<ALG, false, MB, PE><<<(unsigned)grid, kRelaxThreads, 0, st>>>(A);
+    if (src.compact) relax_go(k_relax<ALG, true, MB, PE>, A, grid, smem, st);                 \
+    else relax_go(k_relax<ALG, false, MB, PE>, A, grid, smem, st);
 #define HYT_RELAX(ALG)                                                                           \
     if (peer && peer->n) { HYT_RELAX_B(ALG, 4, true) }                                           \
     else if (minb >= 6) { HYT_RELAX_B(ALG, 6, false) } else if (minb == 5) { HYT_RELAX_B(ALG, 5, false) } \

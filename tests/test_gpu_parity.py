@@ -395,3 +395,19 @@ def test_relax_hub_block(hyt, hot, engine, algo, gkey):
         assert_pr_close(got, want)
     else:
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("hot_v", [32, 1000, 8192, 16384])
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "pr"])
+def test_hub_block_sizes(hyt, hot_v, algo):
+    """The shared-memory hub block size (relax_hot_v) changes no result."""
+    for gi in (4, 5):
+        gkey = ("rmat", gi)
+        g = gkey_graph(gkey)
+        for engine in ("resident", "hybrid"):
+            got, _, _ = run_gpu(hyt, g, algo, engine=engine, part=65536, relax_hot_v=hot_v, relax_hot=2)
+            want = expected(gkey, algo)
+            if algo == "pr":
+                assert_pr_close(got, want)
+            else:
+                assert np.array_equal(got, want)
