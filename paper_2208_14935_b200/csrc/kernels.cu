@@ -307,7 +307,12 @@ static void relax_go(void (*k)(RelaxArgs), const RelaxArgs &A, uint64_t grid, si
     for (int i = 0; i < ncache; ++i)
         if (cache[i].k == k && cache[i].smem == smem) { per_sm = cache[i].per_sm; break; }
     if (per_sm < 0) {
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+        // raise the dynamic limit only past the 48 KB default (a raised limit can shift
+        // the L1 / shared-memory carveout of every later launch)
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, k);
+        if (fa.sharedSizeBytes + smem > 48 * 1024)
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kRelaxThreads, smem) != cudaSuccess || per_sm < 1)
             per_sm = 1;
         if (ncache < 64) cache[ncache++] = Occ{k, smem, per_sm};
