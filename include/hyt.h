@@ -197,8 +197,9 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   zc_ctas_per_sm [2], relax_minb [4] (__launch_bounds__ min CTAs/SM, 4..6),
  *   relax_hot [1] (hub block ids < relax_hot_v in shared memory: PR delta
  *   accumulation, min-algorithm value copy; 0 off, 1 auto, 2 always),
- *   relax_hot_v [4096] (hub-block vertices, 32..32768; 4 B of dynamic shared
- *   memory each; the persistent grid is capped at what stays resident).
+ *   relax_hot_v [16384] (PR hub-block vertices, 32..32768, 4 B of dynamic
+ *   shared memory each; min-algorithms use at most 4096; the persistent grid
+ *   is capped at what stays resident).
  *   exchange [1] (world > 1): 0 always the dense V-entry
  *   all-reduce; 1 per iteration, all-gather the (id, value) pairs each rank
  *   changed when their bytes (world x max pairs x 8) are below the dense

@@ -7,6 +7,7 @@
 //   (the plan / fill / recompute-queue kernels are in plan.cu)
 #include "hyt_internal.h"
 #include "block_prims.cuh"
+#include <algorithm>
 #include <cstdio>
 
 namespace hyt {
@@ -347,7 +348,10 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     // only when every warp has >= 4 tiles (64 KiB of edges per CTA against the 16 KiB
     // hub-value load); range queues (device-side size) do not qualify.  hot = 2
     // forces it on (tests), 0 turns both off.
-    const uint64_t hv = s.V < (uint64_t)s.hot_v ? s.V : (uint64_t)s.hot_v;
+    // PR accumulates into up to hot_v hubs; min-algorithms copy at most kHotV hub values
+    // (the copy is a per-CTA load, a larger one does not pay: profiles/r01_hot_v.md)
+    const uint64_t hv_cap = s.algo == ALGO_PR ? (uint64_t)s.hot_v : std::min<uint64_t>(s.hot_v, kHotV);
+    const uint64_t hv = s.V < hv_cap ? s.V : hv_cap;
     A.n_hot = 0;
     if (hot && s.algo == ALGO_PR) A.n_hot = (uint32_t)hv;
     else if (hot == 2 || (hot == 1 && !dev_tot && (c_hi - c_lo) >= grid * kWarps * 4 * kTile)) A.n_hot = (uint32_t)hv;
