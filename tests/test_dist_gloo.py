@@ -278,3 +278,95 @@ def test_gloo_peer_push_matches_oracle(algo):
     for _, iters, vals in out:
         assert iters > 0
         assert np.array_equal(vals.astype(np.uint32), want)
+
+
+# --------------------------------------------------------------------------- multi-rank pull BFS
+# The pull iteration's frontier gather on CPU: each rank masks its frontier bitmap to
+# its own vertex range and one SUM all-reduce of the 64-bit words yields the OR (the
+# ranks' bits are disjoint); each rank then pulls its own unvisited vertices with the
+# iteration's level and the usual MIN exchange follows (csrc/engine.cu, csrc/pull.cu).
+
+def _pull_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = _graph(symmetric=True)
+        rr = hyt.rank_range(g.off, 4, 4096, world, rank)
+        lo, hi = rr["v_lo"], rr["v_hi"]
+        V, W = g.V, (g.V + 31) // 32
+        vals = np.full(V, INF, dtype=np.int64)
+        vals[0] = 0
+        front = np.zeros(V, dtype=bool)
+        front[0] = True
+        it, pulls = 0, 0
+        while True:
+            n = torch.tensor([int(front[lo:hi].sum())], dtype=torch.int64)
+            dist.all_reduce(n)
+            if n.item() == 0:
+                break
+            nxt = np.zeros(V, dtype=bool)
+            if it % 2 == 1:            # alternate pull / push iterations
+                own = np.zeros(V, dtype=bool)
+                own[lo:hi] = front[lo:hi]
+                words = np.packbits(np.concatenate([own, np.zeros(64 * ((W + 1) // 2) - V, bool)]),
+                                    bitorder="little").view(np.int64).copy()
+                t = torch.from_numpy(words)
+                dist.all_reduce(t)                          # disjoint bits: the sum is the OR
+                glob = np.unpackbits(t.numpy().view(np.uint8), bitorder="little")[:V].astype(bool)
+                assert np.array_equal(glob, _all_or(front, lo, hi, world, g))
+                for v in range(lo, hi):
+                    if vals[v] != INF:
+                        continue
+                    for k in range(int(g.off[v]), int(g.off[v + 1])):
+                        if glob[int(g.nbr[k])]:
+                            vals[v] = it + 1
+                            nxt[v] = True
+                            break
+                pulls += 1
+            else:
+                for u in np.nonzero(front[lo:hi])[0] + lo:
+                    for k in range(int(g.off[u]), int(g.off[u + 1])):
+                        v = int(g.nbr[k])
+                        if vals[u] + 1 < vals[v]:
+                            vals[v] = vals[u] + 1
+                            nxt[v] = True
+            snap = vals[lo:hi].copy()
+            t = torch.from_numpy(vals)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            vals = t.numpy().copy()
+            front = np.zeros(V, dtype=bool)
+            front[lo:hi] = nxt[lo:hi] | (vals[lo:hi] < snap)
+            it += 1
+        q.put((rank, pulls, vals))
+    finally:
+        dist.destroy_process_group()
+
+
+def _all_or(front, lo, hi, world, g):
+    """every rank's own frontier is needed; here each rank only knows its own, so the
+    check gathers them the slow way (all_gather of the boolean vectors)."""
+    own = torch.from_numpy(np.where(np.arange(g.V) >= lo, 1, 0) * np.where(np.arange(g.V) < hi, 1, 0) *
+                           front.astype(np.int64))
+    outs = [torch.zeros_like(own) for _ in range(world)]
+    dist.all_gather(outs, own)
+    return (sum(o.numpy() for o in outs) > 0)
+
+
+def test_gloo_pull_bfs_frontier_or_matches_oracle():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_pull_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = _graph(symmetric=True)
+    want = oracle.bfs(g.off, g.nbr, 0)
+    for _, pulls, vals in out:
+        assert pulls > 0
+        assert np.array_equal(vals.astype(np.uint32), want)
