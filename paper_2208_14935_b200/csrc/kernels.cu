@@ -318,9 +318,12 @@ static void relax_go(void (*k)(RelaxArgs), const RelaxArgs &A, uint64_t grid, si
             per_sm = 1;
         if (ncache < 64) cache[ncache++] = Occ{k, smem, per_sm};
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static thread_local int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+    }
     if (grid > (uint64_t)sms * per_sm) grid = (uint64_t)sms * per_sm;
     k<<<(unsigned)grid, kRelaxThreads, smem, st>>>(A);
 }
