@@ -191,7 +191,10 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
  *   PCIe-3 constants by costs measured on this box -- Eq. 2's CPU term as with
  *   cpu_cost, and Eq. 3 as (active lists x random-request time + further lines
  *   x streamed-line time) / RTT, probed once per process on a pinned buffer
- *   (zc_req_ns / zc_line_ns / link_gbs / thpt_cpt_gbs override the probes);
+ *   (zc_req_ns / zc_line_ns / link_gbs / thpt_cpt_gbs override the probes;
+ *   cal_probe_bytes [4 GiB, >= 256 MiB] sizes the pinned probe buffer, which is
+ *   halved down to 256 MiB if the host cannot pin it; if nothing can be pinned
+ *   the rates measured on the B200 pool are used and the run proceeds);
  *   0 is the paper's rule with its PCIe-3 constants.
  *   Kernel tuning (no effect on results): relax_ctas_per_sm [4],
  *   zc_ctas_per_sm [2], relax_minb [4] (__launch_bounds__ min CTAs/SM, 4..6),

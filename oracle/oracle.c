@@ -264,8 +264,16 @@ int oracle_check_sssp(uint64_t V, const uint64_t *off, const uint32_t *nbr, cons
     return rc;
 }
 
-/* CC certificate on a symmetric graph: label equal across every edge;     */
-/* label(v) <= v; label(label(v)) == label(v) (the label is a member).     */
+/* CC certificate on a symmetric graph (label = minimum  */
+/* caller id of the component).  Complete, O(V + E):                        */
+/*   1. label(u) <= u for every u, and label equal across every edge;       */
+/*   2. from every root r (label(r) == r) a BFS over the edges reaches only */
+/*      vertices labelled r, and marks them;                                */
+/*   3. every vertex is marked.                                             */
+/* (2)+(3) make each label class exactly one component (a class split into  */
+/* two components leaves the part without its root unmarked -- e.g. the     */
+/* merged labelling {0-1},{2-3} -> [0,0,0,0] fails at 3); with (1) the root */
+/* is below every member, so it is the component's minimum id.              */
 int oracle_check_cc(uint64_t V, const uint64_t *off, const uint32_t *nbr, const uint32_t *label) {
     for (uint64_t u = 0; u < V; ++u) {
         if (label[u] > u) return 1;
@@ -273,7 +281,29 @@ int oracle_check_cc(uint64_t V, const uint64_t *off, const uint32_t *nbr, const 
         for (uint64_t k = off[u]; k < off[u + 1]; ++k)
             if (label[nbr[k]] != label[u]) return 3;
     }
-    return 0;
+    uint8_t *seen = (uint8_t *)calloc(V ? V : 1, 1);
+    uint32_t *queue = (uint32_t *)malloc((V ? V : 1) * sizeof(uint32_t));
+    if (!seen || !queue) { free(seen); free(queue); return -2; }
+    int rc = 0;
+    for (uint64_t r = 0; r < V && !rc; ++r) {
+        if (label[r] != r || seen[r]) continue;
+        uint64_t head = 0, tail = 0;
+        seen[r] = 1;
+        queue[tail++] = (uint32_t)r;
+        while (head < tail && !rc) {
+            uint32_t u = queue[head++];
+            for (uint64_t k = off[u]; k < off[u + 1]; ++k) {
+                uint32_t v = nbr[k];
+                if (label[v] != r) { rc = 3; break; }
+                if (!seen[v]) { seen[v] = 1; queue[tail++] = v; }
+            }
+        }
+    }
+    for (uint64_t v = 0; v < V && !rc; ++v)
+        if (!seen[v]) rc = 4;
+    free(seen);
+    free(queue);
+    return rc;
 }
 
 /* PR: L1 norm of T(r) - r with T(r) = (1-d) + d P^T r, and sum of r.       */

@@ -117,6 +117,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "cost_model") { integral(); in(0, 1); p.cost_model = (int)v; }
         else if (k == "zc_req_ns") { in(0, 1e6); p.zc_req_ns = v; g->est_zc_req_ns = v; }
         else if (k == "zc_line_ns") { in(0, 1e6); p.zc_line_ns = v; g->est_zc_line_ns = v; }
+        else if (k == "cal_probe_bytes") { integral(); in(256.0 * (1 << 20), 1e12); p.cal_probe_bytes = (uint64_t)v; }
         else if (k == "thpt_cpt_gbs") { in(0, 1e6); p.thpt_cpt_gbs = v; g->est_cpt_gbs = v; }
         else if (k == "link_gbs") { in(0, 1e6); p.link_gbs = v; g->est_link_gbs = v; }
         else if (k == "direction") { integral(); in(0, 2); p.direction = (int)v; }
@@ -167,7 +168,7 @@ int hyt_get_perm(hyt_graph *g, uint32_t *new_id, uint64_t count) {
         HYT_REQUIRE(g->loaded, HYT_ESTATE, "no graph loaded");
         HYT_REQUIRE(count == g->V, HYT_EINVAL, "count != V");
         HYT_CUDA(cudaSetDevice(g->device));
-        HYT_CUDA(cudaMemcpy(new_id, g->new_id_d, g->V * 4, cudaMemcpyDeviceToHost));
+        HYT_CUDA(copy_sync(new_id, g->new_id_d, g->V * 4, g->main));
     })
 }
 

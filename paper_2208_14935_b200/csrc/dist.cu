@@ -104,7 +104,7 @@ static void local_allreduce(hyt_graph *g, void *buf, uint64_t n, RedOp op, cudaS
     const uint64_t esz = (op == RED_SUM_U64 || op == RED_MAX_U64) ? 8 : 4, bytes = n * esz;
     HYT_CUDA(cudaStreamSynchronize(st));
     G.slot[g->rank].resize(bytes);
-    HYT_CUDA(cudaMemcpy(G.slot[g->rank].data(), buf, bytes, cudaMemcpyDeviceToHost));
+    HYT_CUDA(copy_sync(G.slot[g->rank].data(), buf, bytes, st));
     local_barrier(G);
     if (g->rank == 0) {    // reduce in rank order (a fixed order: f32 sums are reproducible)
         G.result = G.slot[0];
@@ -127,7 +127,7 @@ static void local_allreduce(hyt_graph *g, void *buf, uint64_t n, RedOp op, cudaS
         }
     }
     local_barrier(G);
-    HYT_CUDA(cudaMemcpy(buf, G.result.data(), bytes, cudaMemcpyHostToDevice));
+    HYT_CUDA(copy_sync(buf, G.result.data(), bytes, st));
     local_barrier(G);      // nobody starts the next reduction before all have read this one
 }
 
@@ -137,10 +137,10 @@ static void local_allgather(hyt_graph *g, const void *send, void *recv, uint64_t
     const uint64_t bytes = n * 4;
     HYT_CUDA(cudaStreamSynchronize(st));
     G.slot[g->rank].resize(bytes);
-    HYT_CUDA(cudaMemcpy(G.slot[g->rank].data(), send, bytes, cudaMemcpyDeviceToHost));
+    HYT_CUDA(copy_sync(G.slot[g->rank].data(), send, bytes, st));
     local_barrier(G);
     for (int r = 0; r < G.world; ++r)
-        HYT_CUDA(cudaMemcpy((uint8_t *)recv + (uint64_t)r * bytes, G.slot[r].data(), bytes, cudaMemcpyHostToDevice));
+        HYT_CUDA(copy_sync((uint8_t *)recv + (uint64_t)r * bytes, G.slot[r].data(), bytes, st));
     local_barrier(G);
 }
 
@@ -169,7 +169,7 @@ void dist_share_ptrs(hyt_graph *g, void *const *mine, int nptr, void **all, std:
     uint8_t *dsend = nullptr, *drecv = nullptr;
     HYT_CUDA(cudaMalloc(&dsend, hb * nptr));
     HYT_CUDA(cudaMalloc(&drecv, hb * nptr * g->world));
-    HYT_CUDA(cudaMemcpy(dsend, h.data(), hb * nptr, cudaMemcpyHostToDevice));
+    HYT_CUDA(copy_sync(dsend, h.data(), hb * nptr, st));
     HYT_NCCL(nccl().AllGather(dsend, drecv, hb * nptr / 4, ncclUint32, g->nccl_comm, st));
     std::vector<cudaIpcMemHandle_t> hall((size_t)nptr * g->world);
     HYT_CUDA(cudaMemcpyAsync(hall.data(), drecv, hb * nptr * g->world, cudaMemcpyDeviceToHost, st));

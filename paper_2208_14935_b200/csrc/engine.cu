@@ -363,7 +363,7 @@ static void fill_cache(hyt_graph *g, RunCtx *c, uint64_t p_hi_cache) {
     const uint64_t c0 = chunk_lo(g->off_h[c->bounds[c->p_lo]], c->d1);
     const uint64_t c1 = chunk_hi(g->off_h[c->bounds[p_hi_cache]], c->d1);
     c->cache = dalloc<uint4>(g, c, c1 - c0 + 1, "resident edge cache");
-    HYT_CUDA(cudaMemcpy(c->cache, host_edges(g, c->d1) + c0, (c1 - c0) * 16, cudaMemcpyHostToDevice));
+    HYT_CUDA(copy_sync(c->cache, host_edges(g, c->d1) + c0, (c1 - c0) * 16, g->main));
     c->cache_c0 = c0;
     c->cache_hi = p_hi_cache;
     c->cache_bytes = (c1 - c0) * 16;
@@ -415,9 +415,9 @@ static void build_pull_slices(hyt_graph *g, RunCtx *c) {
     c->hs_v = dalloc<uint32_t>(g, c, c->n_hs, "pull slice vertices");
     c->hs_e0 = dalloc<uint64_t>(g, c, c->n_hs, "pull slice begin");
     c->hs_e1 = dalloc<uint64_t>(g, c, c->n_hs, "pull slice end");
-    HYT_CUDA(cudaMemcpy(c->hs_v, sv.data(), c->n_hs * 4, cudaMemcpyHostToDevice));
-    HYT_CUDA(cudaMemcpy(c->hs_e0, e0.data(), c->n_hs * 8, cudaMemcpyHostToDevice));
-    HYT_CUDA(cudaMemcpy(c->hs_e1, e1.data(), c->n_hs * 8, cudaMemcpyHostToDevice));
+    HYT_CUDA(copy_sync(c->hs_v, sv.data(), c->n_hs * 4, g->main));
+    HYT_CUDA(copy_sync(c->hs_e0, e0.data(), c->n_hs * 8, g->main));
+    HYT_CUDA(copy_sync(c->hs_e1, e1.data(), c->n_hs * 8, g->main));
 }
 
 static RunCtx *build_ctx(hyt_graph *g, int algo) {
@@ -480,10 +480,10 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
             uint64_t *d0 = dalloc<uint64_t>(g, c, c->n_items, "item words lo");
             uint64_t *d1w = dalloc<uint64_t>(g, c, c->n_items, "item words hi");
             uint64_t *df = dalloc<uint64_t>(g, c, c->N + 1, "partition first item");
-            HYT_CUDA(cudaMemcpy(dp, ip.data(), ip.size() * 4, cudaMemcpyHostToDevice));
-            HYT_CUDA(cudaMemcpy(d0, iw0.data(), iw0.size() * 8, cudaMemcpyHostToDevice));
-            HYT_CUDA(cudaMemcpy(d1w, iw1.data(), iw1.size() * 8, cudaMemcpyHostToDevice));
-            HYT_CUDA(cudaMemcpy(df, c->item_first.data(), (c->N + 1) * 8, cudaMemcpyHostToDevice));
+            HYT_CUDA(copy_sync(dp, ip.data(), ip.size() * 4, g->main));
+            HYT_CUDA(copy_sync(d0, iw0.data(), iw0.size() * 8, g->main));
+            HYT_CUDA(copy_sync(d1w, iw1.data(), iw1.size() * 8, g->main));
+            HYT_CUDA(copy_sync(df, c->item_first.data(), (c->N + 1) * 8, g->main));
             c->items.part = dp; c->items.w0 = d0; c->items.w1 = d1w; c->items.first = df;
             c->iagg = dalloc<ItemAgg>(g, c, c->n_items, "item aggregates");
             c->ibase = dalloc<uint64_t>(g, c, 2 * c->n_items, "item bases");
@@ -505,8 +505,8 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->hdr_h = halloc<SegHdr>(c, 1);
         std::vector<uint64_t> t(c->N);
         for (uint64_t i = 0; i < c->N; ++i) t[i] = g->off_h[c->bounds[i + 1]] - g->off_h[c->bounds[i]];
-        HYT_CUDA(cudaMemcpy(c->bounds_d, c->bounds.data(), (c->N + 1) * 8, cudaMemcpyHostToDevice));
-        HYT_CUDA(cudaMemcpy(c->t_d, t.data(), c->N * 8, cudaMemcpyHostToDevice));
+        HYT_CUDA(copy_sync(c->bounds_d, c->bounds.data(), (c->N + 1) * 8, g->main));
+        HYT_CUDA(copy_sync(c->t_d, t.data(), c->N * 8, g->main));
         // ---- staging for filter units: S slots, each holds the largest unit span ----
         uint64_t k = std::max<uint64_t>(1, P.k);
         uint64_t max_span = 0;
@@ -710,31 +710,49 @@ static BoxCal box_calibration(hyt_graph *g) {
     std::lock_guard<std::mutex> lock(g_cal_mu);
     BoxCal &bc = g_cal[g->device & 63];
     if (bc.link_gbs > 0) return bc;
-    // 4 GiB: far larger than the host's last-level cache, so random zero-copy
-    // requests really go to host DRAM (a 256 MiB probe read 5x too fast)
-    const uint64_t hbytes = 4ull << 30;
-    void *h = pinned_alloc(hbytes);
+    // Default 4 GiB (cal_probe_bytes): far larger than the host's last-level cache, so
+    // random zero-copy requests really go to host DRAM (a 256 MiB probe read 5x too
+    // fast).  If the host cannot pin that much, halve down to 256 MiB; if nothing can
+    // be pinned and mapped, fall back to the rates measured on this pool
+    // (profiles/r01_zc_bench.json) instead of failing the run.
+    BoxCal fb;
+    fb.link_gbs = 55.5; fb.zc_req_ns = 14.5; fb.zc_line_ns = 2.5;
+    uint64_t hbytes = std::max<uint64_t>(g->prm.cal_probe_bytes, 256ull << 20);
+    void *h = nullptr;
+    while (!h) {
+        try {
+            h = pinned_alloc(hbytes);
+        } catch (const Err &) {
+            if (hbytes <= (256ull << 20)) { bc = fb; return bc; }
+            hbytes /= 2;
+        }
+    }
+    struct Pin { void *p; ~Pin() { pinned_free(p); } } pin{h};
     uint4 *mapped = nullptr;
-    cudaError_t e = cudaHostGetDevicePointer((void **)&mapped, h, 0);
+    if (cudaHostGetDevicePointer((void **)&mapped, h, 0) != cudaSuccess || !mapped) {
+        cudaGetLastError();
+        bc = fb;
+        return bc;
+    }
     // DMA rate: best of 3 trials of 512 MiB into up to 64 MiB of the handle's arena
     const uint64_t av = g->arena.avail();
     const uint64_t dbytes = std::min<uint64_t>(64ull << 20, av == UINT64_MAX ? (64ull << 20) : av / 2) & ~4095ull;
-    double link = 55.5;   // measured on this pool (profiles/r01_README.md) if there is no room to probe
-    if (dbytes >= (4ull << 20) && e == cudaSuccess) {
+    double link = fb.link_gbs;
+    if (dbytes >= (4ull << 20)) {
         void *d = g->arena.alloc(dbytes, "calibration");
         cudaEvent_t a, b;
-        cudaEventCreate(&a);
-        cudaEventCreate(&b);
+        HYT_CUDA(cudaEventCreate(&a));
+        HYT_CUDA(cudaEventCreate(&b));
         const int reps = (int)std::max<uint64_t>(2, (512ull << 20) / dbytes);
-        cudaMemcpyAsync(d, h, dbytes, cudaMemcpyHostToDevice, g->main);
+        HYT_CUDA(cudaMemcpyAsync(d, h, dbytes, cudaMemcpyHostToDevice, g->main));
         double best = 0;
         for (int trial = 0; trial < 3; ++trial) {
-            cudaEventRecord(a, g->main);
+            HYT_CUDA(cudaEventRecord(a, g->main));
             for (int r = 0; r < reps; ++r)
-                cudaMemcpyAsync(d, (const char *)h + (uint64_t)r * dbytes % (hbytes - dbytes), dbytes,
-                                cudaMemcpyHostToDevice, g->main);
-            cudaEventRecord(b, g->main);
-            cudaEventSynchronize(b);
+                HYT_CUDA(cudaMemcpyAsync(d, (const char *)h + (uint64_t)r * dbytes % (hbytes - dbytes), dbytes,
+                                         cudaMemcpyHostToDevice, g->main));
+            HYT_CUDA(cudaEventRecord(b, g->main));
+            HYT_CUDA(cudaEventSynchronize(b));
             float ms = 0;
             cudaEventElapsedTime(&ms, a, b);
             if (ms > 0) best = std::max(best, (double)dbytes * reps / (ms / 1e3) / 1e9);
@@ -744,23 +762,24 @@ static BoxCal box_calibration(hyt_graph *g) {
         g->arena.release(d);
         if (best > 0) link = best;
     }
-    bc.link_gbs = link;
     uint32_t *sink = (uint32_t *)g->arena.alloc(256, "calibration sink");
     uint64_t lines = 0;
     float ms_r = 0, ms_s = 0;
     for (int trial = 0; trial < 2; ++trial) {   // second trial counts (first warms the mapping)
         ms_r = time_zc_probe(mapped, hbytes / 128, 0, sink, &lines, g->main);
     }
-    bc.zc_req_ns = ms_r * 1e6 / lines;
+    const double req_ns = lines ? ms_r * 1e6 / lines : 0;
     for (int trial = 0; trial < 2; ++trial) ms_s = time_zc_probe(mapped, hbytes / 128, 1, sink, &lines, g->main);
-    bc.zc_line_ns = ms_s * 1e6 / lines;
+    const double line_ns = lines ? ms_s * 1e6 / lines : 0;
+    g->arena.release(sink);
+    HYT_CUDA(cudaGetLastError());
+    bc.link_gbs = link;
+    bc.zc_req_ns = req_ns > 0 ? req_ns : fb.zc_req_ns;
+    bc.zc_line_ns = line_ns > 0 ? line_ns : fb.zc_line_ns;
     // sanity: a random request is never cheaper than a streamed line, and a streamed
     // line is never cheaper than the same 128 B by DMA
     bc.zc_line_ns = std::max(bc.zc_line_ns, 128.0 / link);
     bc.zc_req_ns = std::max(bc.zc_req_ns, bc.zc_line_ns);
-    g->arena.release(sink);
-    pinned_free(h);
-    HYT_CUDA(cudaGetLastError());
     return bc;
 }
 
@@ -838,7 +857,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     const CostParams cp = cost_for(g, c->d1);
     const int mode = P.engine_mode;
     const int prio = P.priority >= 0 ? P.priority : (algo == ALGO_PR ? 2 : 1);
-    const int sms = 148;
+    const int sms = num_sms();
     const int relax_ctas = sms * P.relax_ctas_per_sm, zc_ctas = sms * P.zc_ctas_per_sm;
     const uint4 *edges_host = host_edges(g, c->d1);          // indexed by global chunk
     const uint64_t store_c0 = g->store_c0[c->d1 == 8 ? 1 : 0];
@@ -898,7 +917,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     uint64_t src_int = 0;
     if (algo == ALGO_BFS || algo == ALGO_SSSP) {
         uint32_t x = 0;
-        HYT_CUDA(cudaMemcpy(&x, g->new_id_d + source, 4, cudaMemcpyDeviceToHost));
+        HYT_CUDA(copy_sync(&x, g->new_id_d + source, 4, main));
         src_int = x;
     }
     launch_init_values(s, src_int, g->old_of_d, main);
@@ -1282,7 +1301,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     g->stats.eng_ms[5] = g->recompute_time.ms; g->stats.eng_launches[5] = g->recompute_time.launches;
     {
         uint64_t racc[4] = {0, 0, 0, 0};
-        HYT_CUDA(cudaMemcpy(racc, c->racc, sizeof(racc), cudaMemcpyDeviceToHost));
+        HYT_CUDA(copy_sync(racc, c->racc, sizeof(racc), main));
         g->stats.eng_chunks[5] = racc[1];
         g->stats.eng_edges[5] = racc[2];
     }
@@ -1334,9 +1353,9 @@ void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_par
     RunCtx *c = get_ctx(g, algo);
     DevState s = make_state(g, c);
     uint8_t *act_d = arena_new<uint8_t>(g->arena, g->V, "debug active");
-    HYT_CUDA(cudaMemcpy(act_d, active, g->V, cudaMemcpyHostToDevice));
-    HYT_CUDA(cudaMemset(s.bm_cur, 0, s.W * 4));
-    k_active_to_bitmap<<<148 * 8, 256, 0, g->main>>>(act_d, g->new_id_d, g->V, s.bm_cur);
+    HYT_CUDA(copy_sync(act_d, active, g->V, g->main));
+    HYT_CUDA(cudaMemsetAsync(s.bm_cur, 0, s.W * 4, g->main));
+    k_active_to_bitmap<<<num_sms() * 8, 256, 0, g->main>>>(act_d, g->new_id_d, g->V, s.bm_cur);
     if (algo == ALGO_PR) {   // the plan kernel reads delta for priorities only
         HYT_CUDA(cudaMemsetAsync(s.delta, 0, g->V * 4, g->main));
     }

@@ -82,6 +82,7 @@ struct Params {
     int cost_model = 1;        // 1: Eq. 1-3 with costs calibrated on this box; 0: the paper's PCIe-3 constants
     double zc_req_ns = 0;      // zero-copy random 128-B request time (0 = measure)
     double zc_line_ns = 0;     // zero-copy streamed 128-B line time (0 = measure)
+    uint64_t cal_probe_bytes = 4ull << 30;   // pinned probe buffer of the box calibration (>= 256 MiB)
     int direction = 1;         // BFS/CC on symmetric resident graphs: 0 push, 1 switch (§8f #4), 2 pull
     double pull_alpha = 14, pull_beta = 24, cc_pull_alpha = 2;
     uint64_t pull_heavy = 1024;
@@ -96,6 +97,17 @@ CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio = 0.0, doubl
 // B200 box (tools/pin_bench.cu: 0.34 s vs 3.1 s for 8 GB).
 void *pinned_alloc(uint64_t bytes);
 void pinned_free(void *p);
+
+// Every host<->device copy and memset runs on one of the library's (non-blocking)
+// streams.  A synchronous cudaMemcpy from pageable memory goes through the legacy
+// stream and may return before its DMA lands, and the non-blocking streams are
+// not ordered after it (the round-1 multi-rank race).  copy_sync: enqueue on st,
+// then wait for st, so the copy has landed and later work on st is ordered after it.
+inline cudaError_t copy_sync(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(st);
+}
 
 // Engine timing accumulator (CUDA events per launch, read after the iteration).
 struct EngTime {

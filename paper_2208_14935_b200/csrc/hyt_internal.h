@@ -28,6 +28,20 @@ constexpr int kItemThreads = 256;       // threads per plan / fill / range CTA
 
 constexpr uint32_t kInf = 0xFFFFFFFFu;
 
+// SM count of the current device (148 on B200), queried once per device; grid
+// caps are multiples of it.
+inline int num_sms() {
+    static thread_local int cache[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cache[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
 enum Algo : int { ALGO_BFS = 0, ALGO_SSSP = 1, ALGO_CC = 2, ALGO_PR = 3 };
 enum Eng : int { ENG_NONE = 0, ENG_F = 1, ENG_C = 2, ENG_Z = 3, ENG_R = 4, ENG_COUNT = 5 };
 enum Mode : int { MODE_HYBRID = 0, MODE_FILTER = 1, MODE_COMPACTION = 2, MODE_ZEROCOPY = 3, MODE_RESIDENT = 4, MODE_UM = 5 };

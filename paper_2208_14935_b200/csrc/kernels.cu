@@ -29,7 +29,7 @@ __global__ void k_pr_frontier(const float *__restrict__ delta, uint32_t *__restr
 void launch_pr_frontier(const DevState &s, cudaStream_t st) {
     const uint64_t Vr = (s.V + 31) & ~31ull;
     uint64_t blocks = (Vr + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
     if (blocks == 0) blocks = 1;
     k_pr_frontier<<<(unsigned)blocks, 256, 0, st>>>(s.delta, s.bm_cur, s.V, s.epsilon);
 }
@@ -301,12 +301,16 @@ k_relax(RelaxArgs A) {
 // memory limit once, and cap the persistent grid at what stays resident (a second
 // wave of a grid-stride kernel would double the tail).
 static void relax_go(void (*k)(RelaxArgs), const RelaxArgs &A, uint64_t grid, size_t smem, cudaStream_t st) {
-    struct Occ { void (*k)(RelaxArgs); size_t smem; int per_sm; };
-    static thread_local Occ cache[64];
+    // cached per (device, kernel, smem): the attribute and the occupancy belong to a
+    // device context, and one thread may drive handles on several GPUs
+    struct Occ { int dev; void (*k)(RelaxArgs); size_t smem; int per_sm; };
+    static thread_local Occ cache[128];
     static thread_local int ncache = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
     int per_sm = -1;
     for (int i = 0; i < ncache; ++i)
-        if (cache[i].k == k && cache[i].smem == smem) { per_sm = cache[i].per_sm; break; }
+        if (cache[i].dev == dev && cache[i].k == k && cache[i].smem == smem) { per_sm = cache[i].per_sm; break; }
     if (per_sm < 0) {
         // raise the dynamic limit only past the 48 KB default (a raised limit can shift
         // the L1 / shared-memory carveout of every later launch)
@@ -316,15 +320,9 @@ static void relax_go(void (*k)(RelaxArgs), const RelaxArgs &A, uint64_t grid, si
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kRelaxThreads, smem) != cudaSuccess || per_sm < 1)
             per_sm = 1;
-        if (ncache < 64) cache[ncache++] = Occ{k, smem, per_sm};
+        if (ncache < 128) cache[ncache++] = Occ{dev, k, smem, per_sm};
     }
-    static thread_local int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
-    }
-    if (grid > (uint64_t)sms * per_sm) grid = (uint64_t)sms * per_sm;
+    if (grid > (uint64_t)num_sms() * per_sm) grid = (uint64_t)num_sms() * per_sm;
     k<<<(unsigned)grid, kRelaxThreads, smem, st>>>(A);
 }
 
@@ -400,7 +398,7 @@ __global__ void k_init(DevState s, uint64_t src, const uint32_t *__restrict__ ol
 
 void launch_init_values(const DevState &s, uint64_t src_internal, const uint32_t *old_of, cudaStream_t st) {
     uint64_t blocks = (s.V + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
     if (blocks == 0) blocks = 1;
     k_init<<<(unsigned)blocks, 256, 0, st>>>(s, src_internal, old_of);
 }
@@ -436,7 +434,7 @@ __global__ void k_zc_probe(const uint4 *__restrict__ host, uint64_t nlines, uint
 
 float time_zc_probe(const uint4 *mapped, uint64_t nlines, int mode, uint32_t *sink, uint64_t *lines_read,
                     cudaStream_t st) {
-    const int blocks = 148 * 2, threads = 256;
+    const int blocks = num_sms() * 2, threads = 256;
     const uint64_t per_warp = 2048;    // 4 lines per warp instruction, 16 per step
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -467,7 +465,7 @@ void launch_mark_improved(const uint32_t *val, const uint32_t *snap, uint64_t lo
                           cudaStream_t st) {
     if (hi <= lo) return;
     uint64_t blocks = (hi - lo + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
     k_mark_improved<<<(unsigned)blocks, 256, 0, st>>>(val, snap, lo, hi, bm);
 }
 
@@ -545,19 +543,19 @@ void launch_collect_changed(int pr, uint64_t V, uint64_t lo, uint64_t hi, const 
                             const float *delta, uint2 *pairs, uint64_t cap, unsigned long long *cnt,
                             cudaStream_t st) {
     uint64_t blocks = (V + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
     if (blocks == 0) blocks = 1;
     k_collect_changed<<<(unsigned)blocks, 256, 0, st>>>(pr, V, lo, hi, val, snap, delta, pairs, cap, cnt);
 }
 
 void launch_pad_pairs(uint2 *pairs, const unsigned long long *cnt, uint64_t n, cudaStream_t st) {
-    k_pad_pairs<<<148, 256, 0, st>>>(pairs, cnt, n);
+    k_pad_pairs<<<num_sms(), 256, 0, st>>>(pairs, cnt, n);
 }
 
 void launch_apply_pairs(int pr, const uint2 *pairs, uint64_t n, uint64_t lo, uint64_t hi, uint32_t *val,
                         float *delta, uint32_t *bm_next, cudaStream_t st) {
     uint64_t blocks = (n + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
     if (blocks == 0) return;
     k_apply_pairs<<<(unsigned)blocks, 256, 0, st>>>(pr, pairs, n, lo, hi, val, delta, bm_next);
 }
@@ -572,7 +570,7 @@ __global__ void k_gather_out(const uint32_t *__restrict__ vals, const uint32_t *
 
 void launch_gather_out(const DevState &s, const uint32_t *new_id, void *out_dev, cudaStream_t st) {
     uint64_t blocks = (s.V + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > num_sms() * 16) blocks = num_sms() * 16;
     if (blocks == 0) blocks = 1;
     const uint32_t *vals = s.algo == ALGO_PR ? (const uint32_t *)s.rank : s.val;
     k_gather_out<<<(unsigned)blocks, 256, 0, st>>>(vals, new_id, (uint32_t *)out_dev, s.V);

@@ -228,7 +228,7 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
 // ---------------------------------------------------------------------------
 // host helpers
 // ---------------------------------------------------------------------------
-static unsigned grid_for(uint64_t n, int threads = 256, uint64_t cap = 148 * 32) {
+static unsigned grid_for(uint64_t n, int threads = 256, uint64_t cap = num_sms() * 32) {
     uint64_t b = (n + threads - 1) / threads;
     if (b > cap) b = cap;
     if (b == 0) b = 1;
@@ -420,7 +420,7 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
             for (int pass = 0; pass < 8; ++pass) {
                 const int shift = 56 - 8 * pass;
                 HYT_CUDA(cudaMemsetAsync(hist, 0, 256 * 8, st));
-                k_key_hist<<<grid_for(V, 256, 148 * 8), 256, 0, st>>>(off_old, din, V, prefix, mask, shift, hist);
+                k_key_hist<<<grid_for(V, 256, num_sms() * 8), 256, 0, st>>>(off_old, din, V, prefix, mask, shift, hist);
                 HYT_CUDA(cudaMemcpyAsync(hh.data(), hist, 256 * 8, cudaMemcpyDeviceToHost, st));
                 HYT_CUDA(cudaStreamSynchronize(st));
                 unsigned long long acc = 0;
@@ -504,7 +504,7 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         phase("pin edge store");
 
         if (e_hi > e_lo) {
-            k_relabel_tiles<<<148 * 4, 512, 0, st>>>(V, e_lo, e_hi, off_old, g->off_d, g->old_of_d, g->new_id_d,
+            k_relabel_tiles<<<num_sms() * 4, 512, 0, st>>>(V, e_lo, e_hi, off_old, g->off_d, g->old_of_d, g->new_id_d,
                                                       (const uint32_t *)vn.dev, (const uint32_t *)vw.dev,
                                                       nbr_out - nbase, ew_out ? ew_out - wbase : nullptr);
         }

@@ -431,7 +431,7 @@ __global__ void k_take_delta(DevState s, const uint32_t *__restrict__ qv, const 
 void launch_take_delta(const DevState &s, const QueueBufs &q, uint64_t e_lo, uint64_t e_hi, cudaStream_t st) {
     if (e_hi <= e_lo) return;
     uint64_t blocks = (e_hi - e_lo + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks > num_sms() * 8) blocks = num_sms() * 8;
     k_take_delta<<<(unsigned)blocks, 256, 0, st>>>(s, q.qv, q.qdeg, q.qaux, e_lo, e_hi);
 }
 

@@ -153,7 +153,7 @@ __global__ void k_own_words(const uint32_t *__restrict__ bm, uint32_t *__restric
 
 void launch_own_words(const uint32_t *bm, uint32_t *out, uint64_t nw, uint64_t lo, uint64_t hi, cudaStream_t st) {
     uint64_t grid = (nw + 255) / 256;
-    if (grid > 148ull * 8) grid = 148ull * 8;
+    if (grid > (uint64_t)num_sms() * 8) grid = (uint64_t)num_sms() * 8;
     if (grid == 0) return;
     k_own_words<<<(unsigned)grid, 256, 0, st>>>(bm, out, nw, lo, hi);
 }
@@ -164,10 +164,10 @@ void launch_pull(int algo, const uint64_t *off, const uint32_t *nbr, uint32_t *v
     PullArgs A{off, nbr, val, bm_cur, bm_next, v_lo, v_hi, heavy, lvl};
     const uint64_t n = v_hi > v_lo ? v_hi - v_lo : 0;
     uint64_t grid = (n + 255) / 256;
-    if (grid > 148ull * 8) grid = 148ull * 8;
+    if (grid > (uint64_t)num_sms() * 8) grid = (uint64_t)num_sms() * 8;
     if (grid == 0) grid = 1;
     uint64_t hg = (ns + 7) / 8;
-    if (hg > 148ull * 8) hg = 148ull * 8;
+    if (hg > (uint64_t)num_sms() * 8) hg = (uint64_t)num_sms() * 8;
     if (algo == ALGO_BFS) {
         if (n) k_pull<ALGO_BFS><<<(unsigned)grid, 256, 0, st>>>(A);
         if (ns) k_pull_heavy<ALGO_BFS><<<(unsigned)hg, 256, 0, st>>>(A, sv, e0, e1, ns);

@@ -218,6 +218,44 @@ def test_cc_checker_rejects_mutations():
     assert oracle.check_cc(g.off, g.nbr, bad) != 0
 
 
+def _sym_csr(V, edges):
+    adj = [[] for _ in range(V)]
+    for a, b in edges:
+        adj[a].append(b)
+        adj[b].append(a)
+    off = np.zeros(V + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(x) for x in adj])
+    nbr = np.array([v for x in adj for v in sorted(x)], dtype=np.uint32)
+    return off, nbr
+
+
+def test_cc_checker_golden_cases():
+    """tests/golden/cc_certificate_cases.json: hand-worked valid / invalid labellings,
+    including the merged-components counterexample a local-invariant check accepts."""
+    with open(os.path.join(GOLD, "cc_certificate_cases.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        off, nbr = _sym_csr(c["V"], c["edges"])
+        lab = np.array(c["labels"], dtype=np.uint32)
+        rc = oracle.check_cc(off, nbr, lab)
+        assert (rc == 0) == c["valid"], (c["name"], rc)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_cc_checker_rejects_merged_components(seed):
+    """Relabel a whole component with a smaller root of ANOTHER component: every
+    local invariant (labels equal across edges, label <= v, label is a fixed point)
+    still holds, so only the complete certificate can reject it."""
+    g = hytgen.rmat_csr(11, 2048, 2500, abc=(0.45, 0.22, 0.22), seed=seed, symmetric=True)
+    lab = oracle.cc(g.off, g.nbr)
+    assert oracle.check_cc(g.off, g.nbr, lab) == 0
+    roots = np.nonzero(lab == np.arange(g.V))[0]
+    assert len(roots) >= 2
+    bad = lab.copy()
+    bad[lab == roots[-1]] = roots[0]
+    assert oracle.check_cc(g.off, g.nbr, bad) != 0
+
+
 # ---------------------------------------------------------------- PageRank (O4)
 
 def pr_dense_solve(g, d=D):
