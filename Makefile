@@ -22,7 +22,7 @@ hytgen/libhytgen.so: hytgen/hytgen.c
 	gcc -O3 -march=x86-64-v2 -fPIC -shared -pthread -o $@ $<
 
 oracle/liboracle.so: oracle/oracle.c
-	gcc -O2 -fPIC -shared -o $@ $< -lm
+	gcc -O3 -march=x86-64-v3 -ffp-contract=off -fPIC -shared -pthread -o $@ $< -lm
 
 tools: tools/pin_bench tools/zc_bench tools/scatter_bench
 

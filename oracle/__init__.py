@@ -69,6 +69,8 @@ def _L():
         L.oracle_sssp.argtypes = [u64, vp, vp, vp, u64, vp]
         L.oracle_cc.argtypes = [u64, vp, vp, vp]
         L.oracle_pr_jacobi.argtypes = [u64, vp, vp, ctypes.c_double, ctypes.c_double, i32, vp, ctypes.POINTER(i32)]
+        L.oracle_pr_jacobi_pull.argtypes = [u64, vp, vp, ctypes.c_double, ctypes.c_double, i32, i32, vp,
+                                            ctypes.POINTER(i32)]
         L.oracle_pr_delta.argtypes = [u64, vp, vp, ctypes.c_double, ctypes.c_double, vp, ctypes.POINTER(u64)]
         L.oracle_check_bfs.argtypes = [u64, vp, vp, u64, vp]
         L.oracle_check_sssp.argtypes = [u64, vp, vp, vp, u64, vp]
@@ -143,6 +145,18 @@ def pr_jacobi(off, nbr, d: float = 0.85, tol: float = 1e-13, max_iter: int = 100
     out = np.empty(V, dtype=np.float64)
     it = ctypes.c_int()
     _L().oracle_pr_jacobi(V, _p(off), _p(nbr), d, tol, max_iter, _p(out), ctypes.byref(it))
+    return out, it.value
+
+
+def pr_jacobi_pull(off, nbr, d: float = 0.85, tol: float = 1e-13, max_iter: int = 100000, threads: int = 0):
+    """O4a in pull form over a transposed CSR, vertex range split over POSIX threads
+    (threads = 0: all host cores).  Same map and stopping rule as pr_jacobi; used at
+    the large parity sizes where the single-threaded push form takes minutes."""
+    off, nbr, V = _csr(off, nbr)
+    out = np.empty(V, dtype=np.float64)
+    it = ctypes.c_int()
+    nt = threads or (os.cpu_count() or 1)
+    _L().oracle_pr_jacobi_pull(V, _p(off), _p(nbr), d, tol, max_iter, nt, _p(out), ctypes.byref(it))
     return out, it.value
 
 

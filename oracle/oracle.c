@@ -5,7 +5,7 @@
  * cpu_baseline / --impl reference legs of bench.py may load this library.  The
  * product (paper_2208_14935_b200/) never links, imports or calls it, and it
  * shares no code, header, table or helper with the product: it includes only
- * the C standard library.
+ * the C standard library (and POSIX threads for the pull-form Jacobi O4a').
  *
  * Plain, slow, obviously correct, single-threaded; fp64 for floating point.
  * Citations: P:n = /root/reference/PAPER.md line n (the paper), S:n = SPEC.md
@@ -176,6 +176,80 @@ int oracle_pr_jacobi(uint64_t V, const uint64_t *off, const uint32_t *nbr, doubl
     }
     if (iters_out) *iters_out = it;
     free(acc);
+    return 0;
+}
+
+/* O4a': the same Jacobi map in PULL form, for the large parity sizes:      */
+/*   r_new[v] = (1-d) + d * sum_{u -> v} r[u] / D_o(u)                      */
+/* over a transposed CSR (in-lists, built by a counting sort), with the     */
+/* vertex range split across `threads` POSIX threads.  Every r_new[v] is    */
+/* written by one thread and summed in in-list order, so the result does    */
+/* not depend on the thread count.  Same stopping rule as O4a.              */
+#include <pthread.h>
+typedef struct {
+    uint64_t v0, v1;
+    const uint64_t *ioff; const uint32_t *isrc;
+    const double *share; double *next; double d;
+} pull_job;
+
+static void *pull_range(void *arg) {
+    pull_job *j = (pull_job *)arg;
+    for (uint64_t v = j->v0; v < j->v1; ++v) {
+        double acc = 0.0;
+        for (uint64_t k = j->ioff[v]; k < j->ioff[v + 1]; ++k) acc += j->share[j->isrc[k]];
+        double nv = (1.0 - j->d) + j->d * acc;
+        j->next[v] = nv;
+    }
+    return NULL;
+}
+
+int oracle_pr_jacobi_pull(uint64_t V, const uint64_t *off, const uint32_t *nbr, double d,
+                          double tol, int max_iter, int threads, double *rank, int *iters_out) {
+    if (threads < 1) threads = 1;
+    if (threads > 256) threads = 256;
+    const uint64_t E = off[V];
+    uint64_t *ioff = (uint64_t *)calloc(V + 1, sizeof(uint64_t));
+    uint32_t *isrc = (uint32_t *)malloc((E ? E : 1) * sizeof(uint32_t));
+    uint64_t *fill = (uint64_t *)malloc((V ? V : 1) * sizeof(uint64_t));
+    double *share = (double *)malloc((V ? V : 1) * sizeof(double));
+    double *next = (double *)malloc((V ? V : 1) * sizeof(double));
+    pthread_t *th = (pthread_t *)malloc(threads * sizeof(pthread_t));
+    pull_job *jobs = (pull_job *)malloc(threads * sizeof(pull_job));
+    if (!ioff || !isrc || !fill || !share || !next || !th || !jobs) {
+        free(ioff); free(isrc); free(fill); free(share); free(next); free(th); free(jobs);
+        return -2;
+    }
+    /* transpose: in-degree count, exclusive scan, scatter (sources in increasing u) */
+    for (uint64_t k = 0; k < E; ++k) ioff[nbr[k] + 1] += 1;
+    for (uint64_t v = 0; v < V; ++v) ioff[v + 1] += ioff[v];
+    for (uint64_t v = 0; v < V; ++v) fill[v] = ioff[v];
+    for (uint64_t u = 0; u < V; ++u)
+        for (uint64_t k = off[u]; k < off[u + 1]; ++k) isrc[fill[nbr[k]]++] = (uint32_t)u;
+    for (uint64_t v = 0; v < V; ++v) rank[v] = 1.0 - d;
+    int it = 0;
+    for (; it < max_iter; ++it) {
+        for (uint64_t u = 0; u < V; ++u) {
+            uint64_t deg = off[u + 1] - off[u];
+            share[u] = deg ? rank[u] / (double)deg : 0.0;
+        }
+        for (int t = 0; t < threads; ++t) {
+            jobs[t].v0 = V * (uint64_t)t / (uint64_t)threads;
+            jobs[t].v1 = V * (uint64_t)(t + 1) / (uint64_t)threads;
+            jobs[t].ioff = ioff; jobs[t].isrc = isrc; jobs[t].share = share;
+            jobs[t].next = next; jobs[t].d = d;
+            pthread_create(&th[t], NULL, pull_range, &jobs[t]);
+        }
+        for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+        double diff = 0.0;
+        for (uint64_t v = 0; v < V; ++v) {
+            double dv = fabs(next[v] - rank[v]);
+            if (dv > diff) diff = dv;
+            rank[v] = next[v];
+        }
+        if (diff < tol) { ++it; break; }
+    }
+    if (iters_out) *iters_out = it;
+    free(ioff); free(isrc); free(fill); free(share); free(next); free(th); free(jobs);
     return 0;
 }
 

@@ -1083,7 +1083,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             }
             timed_begin(c, stm, e2, TAG_F);
             launch_relax(s, c->q, H.tile_base[ENG_F], fseg_first, fseg_end, H.chunk_total[ENG_F], c_lo, c_hi,
-                         nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot, ppp);
+                         nullptr, es, relax_ctas, stm, P.relax_hot, ppp);
             timed_end(c, stm, e2);
             if (P.recompute) {   // process the loaded unit exactly once more
                 EvPair e4;
@@ -1091,7 +1091,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 launch_range_queue(s, v_lo, v_hi, c->rb[si], stm);
                 timed_end(c, stm, e4);
                 timed_begin(c, stm, e3, TAG_RECOMP);
-                launch_relax(s, c->rb[si].q, 0, 0, 0, 0, 0, 0, c->rb[si].total, es, relax_ctas, stm, P.relax_minb, P.relax_hot, ppp);
+                launch_relax(s, c->rb[si].q, 0, 0, 0, 0, 0, 0, c->rb[si].total, es, relax_ctas, stm, P.relax_hot, ppp);
                 timed_end(c, stm, e3);
             }
             g->launches += P.recompute ? 4 : 1;
@@ -1110,7 +1110,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 g->launches += 1;
             }
             launch_relax(s, c->q, H.tile_base[ENG_Z], H.ent_base[ENG_Z], H.ent_base[ENG_Z] + H.ent_count[ENG_Z],
-                         H.chunk_total[ENG_Z], 0, H.chunk_total[ENG_Z], nullptr, es, zc_ctas, stm, P.relax_minb, P.relax_hot, ppp);
+                         H.chunk_total[ENG_Z], 0, H.chunk_total[ENG_Z], nullptr, es, zc_ctas, stm, P.relax_hot, ppp);
             timed_end(c, stm, e1);
             g->launches += 1;
             g->eng_chunks[ENG_Z] += H.chunk_total[ENG_Z];
@@ -1148,7 +1148,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 g->launches += 1;
             }
             launch_relax(s, c->q, H.tile_base[ENG_R], H.ent_base[ENG_R], H.ent_base[ENG_R] + H.ent_count[ENG_R],
-                         H.chunk_total[ENG_R], 0, H.chunk_total[ENG_R], nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot, ppp);
+                         H.chunk_total[ENG_R], 0, H.chunk_total[ENG_R], nullptr, es, relax_ctas, stm, P.relax_hot, ppp);
             timed_end(c, stm, e1);
             g->launches += 1;
             g->eng_chunks[ENG_R] += H.chunk_total[ENG_R];
@@ -1190,7 +1190,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 EdgeSrc es{c->cbuf[bi], 0, true};
                 timed_begin(c, stm, e2, TAG_C);
                 launch_relax(s, c->q, H.tile_base[ENG_C], H.ent_base[ENG_C], H.ent_base[ENG_C] + nC, total, w_lo,
-                             w_hi, nullptr, es, relax_ctas, stm, P.relax_minb, P.relax_hot, ppp);
+                             w_hi, nullptr, es, relax_ctas, stm, P.relax_hot, ppp);
                 timed_end(c, stm, e2);
                 g->launches += 1;
             }

@@ -66,13 +66,12 @@ struct Params {
     uint64_t max_iters = 1000;
     int gather_threads = 0;
     uint64_t compaction_buffer_bytes = 0;
-    int zc_ctas_per_sm = 2;
-    int relax_ctas_per_sm = 4;
+    int zc_ctas_per_sm = 1;     // 512-thread CTAs
+    int relax_ctas_per_sm = 2;  // 512-thread CTAs
     int exchange = 1;          // multi-GPU: 0 dense, 1 sparse when cheaper (§8f #3), 2 sparse when it fits,
                                // 3 fused peer push (relax writes remote destinations into their owner's memory)
     int relax_hot = 1;         // hub block in smem (PR Δ accumulation / min-algorithm value copy): 0 off, 1 auto, 2 always
-    uint64_t relax_hot_v = 16384;   // PR hub-block vertices in shared memory (64 KB; min-algorithms cap at kHotV)
-    int relax_minb = 4;        // __launch_bounds__ min CTAs/SM of the relax kernel (4: 64 regs, 5: 51, 6: 42)
+    uint64_t relax_hot_v = 8192;    // PR hub-block vertices in shared memory (8 B each: 64 KB; min-algorithms cap at kHotV)
     int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
     uint64_t edge_cache_bytes = 0;   // cap on the cache (0 = whatever the budget leaves)
     int cpu_cost = 0;          // 1: include Eq. 2's CPU term with Thpt_cpt calibrated on this box

@@ -16,7 +16,8 @@ namespace hyt {
 // line (the EMOGI "merged and aligned" access).
 // ---------------------------------------------------------------------------
 constexpr int kChunkBytes = 16;
-constexpr int kRelaxThreads = 256;      // threads per relax CTA (8 independent warps)
+constexpr int kRelaxThreads = 512;      // threads per relax CTA (16 independent warps sharing one hub block)
+constexpr int kRelaxMinBlocks = 2;      // 2 x 512 threads per SM: 64 registers per thread
 constexpr int kChunksPerThread = 4;     // 16-byte loads in flight per lane
 constexpr int kTile = 32 * kChunksPerThread;   // chunks per WARP tile (2 KiB of edges)
 #ifndef HYT_HOTV
@@ -196,7 +197,7 @@ struct EdgeSrc {
 // with seg_chunks chunks; dev_tot (range queues) overrides seg_end/seg_chunks/c_hi.
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
-                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb = 4, int hot = 1,
+                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int hot = 1,
                   const PeerPush *peer = nullptr);
 void launch_take_delta(const DevState &s, const QueueBufs &q, uint64_t e_lo, uint64_t e_hi, cudaStream_t st);
 void launch_range_queue(const DevState &s, uint64_t v_lo, uint64_t v_hi, RangeBufs r, cudaStream_t st);

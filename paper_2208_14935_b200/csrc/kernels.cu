@@ -113,21 +113,49 @@ __device__ __forceinline__ bool peer_remote(const PeerPush &pp, uint32_t d) {
     return (uint64_t)d < pp.lo || (uint64_t)d >= pp.hi;
 }
 
-template <int ALGO, bool COMPACT, int MINB, bool PEER>
-__global__ void __launch_bounds__(kRelaxThreads, MINB)
+// Per-warp staging of the <= kTile+1 queue entries overlapping one tile, 16 B per
+// entry (the round-1 layout held prefix / first edge as u64 and spent 24 B):
+//   a[e]  = absolute chunk address of TILE POSITION 0 for entry e, so tile position
+//           p of the entry is chunk a[e] + p (one 64-bit add per chunk);
+//   lh[e] = the entry's first / end edge SLOT relative to tile position 0, as two
+//           int16 (clamped to [-EPC, (kTile+1)*EPC]: only [0, EPC) matters for any p);
+//           at position p the valid slots of the chunk are
+//           [max(0, lo - p*EPC), min(EPC, hi - p*EPC));
+//   src[e] = the pushed value (PR: f32 contribution d*delta/D_o; else u32 value).
+struct WarpStage {
+    uint64_t a[kTile + 1];
+    uint32_t lh[kTile + 1];
+    uint32_t src[kTile + 1];
+    uint32_t mask[kChunksPerThread];
+};
+
+// PR hub block in fixed point: x in units of 2^-32 as a 64-bit (hi, lo) pair of u32
+// words, so every add is a native shared-memory ATOMS.ADD (an f32 or u64 atomicAdd
+// on shared memory compiles to a CAS spin loop on sm_100a, which serialises the
+// lanes of a warp that hit the same hub).  The carry out of lo is detected from
+// the returned old value and added to hi.  Range: 2^32 per hub per CTA, above any
+// mass one launch can push (sum of pushes <= sum of delta <= V < 2^32).  Rounding:
+// <= 2^-33 absolute per add, i.e. at or below f32 rounding for any partial sum
+// >= 2^-9; the flush converts the pair back to f32 once per CTA.
+__device__ __forceinline__ void hub_add_fx(uint32_t *lo, uint32_t *hi, uint32_t d, uint32_t xlo, uint32_t xhi) {
+    if (xhi) atomicAdd(&hi[d], xhi);
+    const uint32_t old = atomicAdd(&lo[d], xlo);
+    if (old + xlo < old) atomicAdd(&hi[d], 1u);
+}
+
+template <int ALGO, bool COMPACT, bool PEER>
+__global__ void __launch_bounds__(kRelaxThreads, kRelaxMinBlocks)
 k_relax(RelaxArgs A) {
     constexpr uint32_t D1 = (ALGO == ALGO_SSSP) ? 8u : 4u;
     constexpr int EPC = 16 / D1;                  // edge records per chunk
     constexpr bool PR = (ALGO == ALGO_PR);
-    __shared__ uint64_t s_pre[kWarps][kTile + 1];
-    __shared__ uint64_t s_beg[kWarps][kTile + 1];
-    __shared__ uint32_t s_deg[kWarps][kTile + 1];
-    __shared__ uint32_t s_src[kWarps][kTile + 1];
-    __shared__ uint32_t s_mask[kWarps][kChunksPerThread];
-    extern __shared__ uint32_t s_hotw[];          // hub block (dynamic, n_hot words): PR Δ accumulators; else hub values
-    float *s_hot = reinterpret_cast<float *>(s_hotw);
+    __shared__ WarpStage s_st[kWarps];
+    // hub block (dynamic): PR = n_hot lo words then n_hot hi words (fixed point);
+    // min-algorithms = n_hot hub values
+    extern __shared__ uint32_t s_hotw[];
     const DevState &S = A.s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    WarpStage &W = s_st[w];
     const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
 
     uint64_t c_lo = A.c_lo, c_hi = A.c_hi, seg_chunks = A.seg_chunks, seg_end = A.seg_end;
@@ -137,9 +165,13 @@ k_relax(RelaxArgs A) {
         c_hi = seg_chunks;
     }
     const uint32_t n_hot = A.n_hot;
+    uint32_t *const s_lo = s_hotw, *const s_hi = s_hotw + n_hot;
     if (n_hot) {
-        for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x)
-            s_hotw[i] = PR ? 0u : ld_keep(&S.val[i], pol_keep);
+        if (PR) {
+            for (uint32_t i = threadIdx.x; i < 2 * n_hot; i += blockDim.x) s_hotw[i] = 0u;
+        } else {
+            for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x) s_hotw[i] = ld_keep(&S.val[i], pol_keep);
+        }
         __syncthreads();
     }
     if (c_hi > c_lo) {
@@ -153,41 +185,44 @@ k_relax(RelaxArgs A) {
             const uint64_t k0 = A.tile[t];
             const uint64_t k1 = (t + 1 < ntiles_seg) ? (uint64_t)A.tile[t + 1] : seg_end - 1;
             const int ne = (int)(k1 - k0 + 1);
-            if (lane < kChunksPerThread) s_mask[w][lane] = 0u;
+            if (lane < kChunksPerThread) W.mask[lane] = 0u;
             __syncwarp();
             for (int e = lane; e < ne; e += 32) {
                 const uint64_t k = k0 + e;
-                const uint64_t pre = A.qpre[k];
-                s_pre[w][e] = pre;
-                s_beg[w][e] = A.qbeg[k];
-                s_deg[w][e] = A.qdeg[k];
-                s_src[w][e] = PR ? __float_as_uint(A.qaux[k]) : ld_keep(&S.val[A.qv[k]], pol_keep);
+                const uint64_t pre = A.qpre[k], beg = A.qbeg[k];
+                const uint32_t deg = A.qdeg[k];
+                const int64_t rel = (int64_t)pre - (int64_t)tb;       // entry start - tile start (chunks)
+                W.a[e] = chunk_lo(beg, D1) - (uint64_t)rel;
+                const int64_t lo = (int64_t)(beg % EPC) + rel * EPC, hi = lo + deg;
+                const int64_t cap = (int64_t)(kTile + 1) * EPC;
+                const int32_t l16 = (int32_t)(lo < -EPC ? -EPC : lo);
+                const int32_t h16 = (int32_t)(hi > cap ? cap : hi);
+                W.lh[e] = ((uint32_t)l16 & 0xFFFFu) | ((uint32_t)h16 << 16);
+                W.src[e] = PR ? __float_as_uint(A.qaux[k]) : ld_keep(&S.val[A.qv[k]], pol_keep);
                 // 128-bit map of the tile positions where an entry starts (the entry
                 // covering the tile's first chunk starts at position 0)
-                const uint64_t pos = pre > tb ? pre - tb : 0;
-                if (pos < (uint64_t)kTile) atomicOr(&s_mask[w][pos >> 5], 1u << (pos & 31));
+                const uint64_t pos = rel > 0 ? (uint64_t)rel : 0;
+                if (pos < (uint64_t)kTile) atomicOr(&W.mask[pos >> 5], 1u << (pos & 31));
             }
             __syncwarp();
             uint4 data[kChunksPerThread];
             int ent[kChunksPerThread];
-            uint64_t absc[kChunksPerThread];
             // lane L's r-th chunk is tile position 32 r + L: its entry index is the
             // number of starts at positions <= 32 r + L, minus one
             const uint32_t le = 0xFFFFFFFFu >> (31 - lane);
             int before = 0;
 #pragma unroll
             for (int r = 0; r < kChunksPerThread; ++r) {
-                const uint32_t m = s_mask[w][r];
-                const uint64_t c = tb + (uint64_t)r * 32 + lane;
+                const uint32_t m = W.mask[r];
+                const int p = r * 32 + lane;
+                const uint64_t c = tb + p;
                 const int e = before + __popc(m & le) - 1;
                 before += __popc(m);
                 ent[r] = -1;
                 if (c >= cb && c < ce) {
-                    const uint64_t ac = chunk_lo(s_beg[w][e], D1) + (c - s_pre[w][e]);
-                    const uint4 *p = COMPACT ? (A.base + (c - c_lo)) : (A.base + ((int64_t)ac - A.shift));
-                    data[r] = ld_stream(p, pol_stream);
+                    const uint4 *ptr = COMPACT ? (A.base + (c - c_lo)) : (A.base + ((int64_t)(W.a[e] + p) - A.shift));
+                    data[r] = ld_stream(ptr, pol_stream);
                     ent[r] = e;
-                    absc[r] = ac;
                 }
             }
             if constexpr (PR) {
@@ -195,18 +230,19 @@ k_relax(RelaxArgs A) {
                 for (int r = 0; r < kChunksPerThread; ++r) {
                     if (ent[r] < 0) continue;
                     const int e = ent[r];
-                    const uint64_t base = absc[r] * EPC, beg = s_beg[w][e];
-                    // valid edge slots of this chunk: [lo, hi) (32-bit after one 64-bit step)
-                    const int lo = beg > base ? (int)(beg - base) : 0;
-                    const uint64_t end = beg + s_deg[w][e];
-                    const int hi = end - base < (uint64_t)EPC ? (int)(end - base) : EPC;
-                    const float x = __uint_as_float(s_src[w][e]);
+                    const int p = r * 32 + lane;
+                    const uint32_t lh = W.lh[e];
+                    const int lo = (int)(int16_t)(lh & 0xFFFFu) - p * EPC;
+                    const int hi = (int)(int16_t)(lh >> 16) - p * EPC;
+                    const float x = __uint_as_float(W.src[e]);
+                    const unsigned long long X = __float2ull_rn(x * 4294967296.0f);
+                    const uint32_t xlo = (uint32_t)X, xhi = (uint32_t)(X >> 32);
                     const uint32_t words[4] = {data[r].x, data[r].y, data[r].z, data[r].w};
 #pragma unroll
                     for (int qd = 0; qd < EPC; ++qd) {
                         if (qd < lo || qd >= hi) continue;
                         const uint32_t dst = words[qd];
-                        if (dst < n_hot) atomicAdd(&s_hot[dst], x);
+                        if (dst < n_hot) hub_add_fx(s_lo, s_hi, dst, xlo, xhi);
                         else if (PEER && peer_remote(A.pp, dst)) atomicAdd(&A.pp.delta[peer_owner(A.pp, dst)][dst], x);
                         else red_add_keep(&S.delta[dst], x, pol_keep);
                     }
@@ -224,11 +260,11 @@ k_relax(RelaxArgs A) {
                         uint32_t src = 0;
                         if (ent[r] >= 0) {
                             const int e = ent[r];
-                            const uint64_t base = absc[r] * EPC, beg = s_beg[w][e];
-                            lo = beg > base ? (int)(beg - base) : 0;
-                            const uint64_t end = beg + s_deg[w][e];
-                            hi = end - base < (uint64_t)EPC ? (int)(end - base) : EPC;
-                            src = s_src[w][e];
+                            const int p = r * 32 + lane;
+                            const uint32_t lh = W.lh[e];
+                            lo = (int)(int16_t)(lh & 0xFFFFu) - p * EPC;
+                            hi = (int)(int16_t)(lh >> 16) - p * EPC;
+                            src = W.src[e];
                         }
                         const uint32_t words[4] = {data[r].x, data[r].y, data[r].z, data[r].w};
 #pragma unroll
@@ -289,8 +325,9 @@ k_relax(RelaxArgs A) {
     if (PR && n_hot) {
         __syncthreads();
         for (uint32_t i = threadIdx.x; i < n_hot; i += blockDim.x) {
-            const float x = s_hot[i];
-            if (x == 0.0f) continue;
+            const uint64_t X = ((uint64_t)s_hi[i] << 32) | s_lo[i];
+            if (X == 0) continue;
+            const float x = (float)((double)X * (1.0 / 4294967296.0));
             if (PEER && peer_remote(A.pp, i)) atomicAdd(&A.pp.delta[peer_owner(A.pp, i)][i], x);
             else atomicAdd(&S.delta[i], x);
         }
@@ -328,7 +365,7 @@ static void relax_go(void (*k)(RelaxArgs), const RelaxArgs &A, uint64_t grid, si
 
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
                   uint64_t seg_end, uint64_t seg_chunks, uint64_t c_lo, uint64_t c_hi,
-                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int minb, int hot,
+                  const uint64_t *dev_tot, EdgeSrc src, int max_ctas, cudaStream_t st, int hot,
                   const PeerPush *peer) {
     RelaxArgs A;
     A.s = s; A.qv = q.qv; A.qpre = q.qpre; A.qbeg = q.qbeg; A.qdeg = q.qdeg; A.qaux = q.qaux;
@@ -356,14 +393,13 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     A.n_hot = 0;
     if (hot && s.algo == ALGO_PR) A.n_hot = (uint32_t)hv;
     else if (hot == 2 || (hot == 1 && !dev_tot && (c_hi - c_lo) >= grid * kWarps * 4 * kTile)) A.n_hot = (uint32_t)hv;
-    const size_t smem = (size_t)A.n_hot * 4;
-#define HYT_RELAX_B(ALG, MB, PE)                                                                 \
-    if (src.compact) relax_go(k_relax<ALG, true, MB, PE>, A, grid, smem, st);                 \
-    else relax_go(k_relax<ALG, false, MB, PE>, A, grid, smem, st);
+    const size_t smem = (size_t)A.n_hot * (s.algo == ALGO_PR ? 8 : 4);   // PR: fixed-point (lo, hi) pairs
+#define HYT_RELAX_B(ALG, PE)                                                                     \
+    if (src.compact) relax_go(k_relax<ALG, true, PE>, A, grid, smem, st);                     \
+    else relax_go(k_relax<ALG, false, PE>, A, grid, smem, st);
 #define HYT_RELAX(ALG)                                                                           \
-    if (peer && peer->n) { HYT_RELAX_B(ALG, 4, true) }                                           \
-    else if (minb >= 6) { HYT_RELAX_B(ALG, 6, false) } else if (minb == 5) { HYT_RELAX_B(ALG, 5, false) } \
-    else { HYT_RELAX_B(ALG, 4, false) }
+    if (peer && peer->n) { HYT_RELAX_B(ALG, true) }                                              \
+    else { HYT_RELAX_B(ALG, false) }
     switch (s.algo) {
         case ALGO_BFS: HYT_RELAX(ALGO_BFS); break;
         case ALGO_SSSP: HYT_RELAX(ALGO_SSSP); break;

@@ -397,7 +397,7 @@ def test_relax_hub_block(hyt, hot, engine, algo, gkey):
         assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("hot_v", [32, 1000, 8192, 16384])
+@pytest.mark.parametrize("hot_v", [32, 1000, 8192, 12288])
 @pytest.mark.parametrize("algo", ["bfs", "sssp", "pr"])
 def test_hub_block_sizes(hyt, hot_v, algo):
     """The shared-memory hub block size (relax_hot_v) changes no result."""

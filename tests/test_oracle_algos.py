@@ -278,6 +278,28 @@ def test_pr_vs_dense_solve(seed):
     assert np.max(np.abs(rd - want) / want) < 1e-10
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_pr_pull_vs_dense_solve(seed):
+    """O4a' (pull-form Jacobi over a transposed CSR, threaded) against the linear
+    solve directly, on tiny graphs with dangling vertices and duplicate edges."""
+    g = random_tiny(seed + 700, p=0.15)
+    want = pr_dense_solve(g)
+    for nt in (1, 3):
+        got, _ = oracle.pr_jacobi_pull(g.off, g.nbr, tol=1e-14, threads=nt)
+        assert np.max(np.abs(got - want) / want) < 1e-11
+
+
+def test_pr_pull_thread_count_invariant():
+    """Each vertex is summed by one thread in in-list order: the result is the same
+    bit for bit for any thread count, and equals the push form to rounding."""
+    g = hytgen.rmat_csr(13, 8192, 120000, seed=21)
+    a, ia = oracle.pr_jacobi_pull(g.off, g.nbr, tol=1e-12, threads=1)
+    b, ib = oracle.pr_jacobi_pull(g.off, g.nbr, tol=1e-12, threads=7)
+    assert ia == ib and np.array_equal(a, b)
+    c, _ = oracle.pr_jacobi(g.off, g.nbr, tol=1e-12)
+    assert np.max(np.abs(a - c) / c) < 1e-10
+
+
 def test_pr_closed_forms():
     # directed cycle -> all 1 (unnormalised fixed point, SURVEY O4)
     n = 7
