@@ -4,9 +4,9 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -O3 --expt-relaxed-constexpr $(EXTRA)
 SRC_DIR := paper_2208_14935_b200/csrc
 LIB := paper_2208_14935_b200/lib/libhyt.so
-SRCS := $(SRC_DIR)/plan.cu $(SRC_DIR)/kernels.cu $(SRC_DIR)/load.cu $(SRC_DIR)/engine.cu $(SRC_DIR)/api.cu $(SRC_DIR)/dist.cu $(SRC_DIR)/pull.cu
+SRCS := $(SRC_DIR)/plan.cu $(SRC_DIR)/kernels.cu $(SRC_DIR)/load.cu $(SRC_DIR)/engine.cu $(SRC_DIR)/api.cu $(SRC_DIR)/dist.cu $(SRC_DIR)/pull.cu $(SRC_DIR)/scan.cu
 OBJS := $(patsubst $(SRC_DIR)/%.cu,build/%.o,$(SRCS))
-HDRS := $(SRC_DIR)/hyt_internal.h $(SRC_DIR)/block_prims.cuh $(SRC_DIR)/graph.h include/hyt.h
+HDRS := $(SRC_DIR)/scan.h $(SRC_DIR)/hyt_internal.h $(SRC_DIR)/block_prims.cuh $(SRC_DIR)/graph.h include/hyt.h
 
 all: $(LIB) hytgen/libhytgen.so oracle/liboracle.so
 

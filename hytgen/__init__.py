@@ -43,6 +43,10 @@ def _L():
         lib.hytgen_weights.argtypes = [u64, u64p, u32p, u64, u32p]
         lib.hytgen_degree_stats.argtypes = [u64, u64p] + [ctypes.POINTER(ctypes.c_uint64)] * 4
         lib.hytgen_degree_stats.restype = None
+        i32 = ctypes.c_int
+        lib.hytgen_rmat_degrees.argtypes = [i32, u64, u64, dbl, dbl, dbl, u64, i32, u64, u64, u32p, u32p]
+        lib.hytgen_rmat_rows.argtypes = [i32, u64, u64, dbl, dbl, dbl, u64, i32, u32p, u64, u64p, u32p, u64]
+        lib.hytgen_weights_rows.argtypes = [u64, u32p, u64p, u32p, u64, u32p]
         _lib = lib
     return _lib
 
@@ -173,3 +177,49 @@ def make(name: str, shift: int = 0, weighted: bool = False) -> Graph:
     return rmat_csr(c["scale"], c["V"], c["E"], c["abc"], c["seed"], c["symmetric"],
                     weighted=weighted, weight_seed=c["seed"] + 1000,
                     name=name if not shift else f"{name}>>{shift}")
+
+
+# ---------------------------------------------------------------- per-rank shards
+# (SURVEY §7.2 #6): no process ever holds the whole graph.  Every edge is a pure
+# function of its index, so a rank counts the degrees of its slice of edge indices
+# (the caller sums the slices over ranks) and regenerates every edge to keep the
+# rows of the vertices it owns.
+
+def recipe(name: str, shift: int = 0) -> dict:
+    return scaled(name, shift) if shift else dict(CONFIGS[name])
+
+
+def rmat_degrees(c: dict, e0: int, e1: int, out_deg=None, in_deg=None):
+    """Add the stored out-/in-degrees of edges [e0, e1) of recipe c into u32[V] arrays."""
+    V = c["V"]
+    if out_deg is None:
+        out_deg = np.zeros(V, dtype=np.uint32)
+    if in_deg is None:
+        in_deg = np.zeros(V, dtype=np.uint32)
+    rc = _L().hytgen_rmat_degrees(c["scale"], V, c["E"], *c["abc"], c["seed"], int(c["symmetric"]), e0, e1,
+                                  _p(out_deg), _p(in_deg))
+    if rc != 0:
+        raise ValueError(f"hytgen_rmat_degrees rc={rc}")
+    return out_deg, in_deg
+
+
+def rmat_rows(c: dict, rows: np.ndarray, out_deg: np.ndarray, weighted: bool = False):
+    """The CSR rows of original vertices `rows` (in that order) of recipe c: returns
+    (off_local u64[n+1], nbr u32[...], w u32[...] | None), each row sorted ascending
+    exactly as in rmat_csr's full CSR; neighbour ids stay original."""
+    rows = np.ascontiguousarray(rows, dtype=np.uint32)
+    n = len(rows)
+    slot = np.full(c["V"], 0xFFFFFFFF, dtype=np.uint32)
+    slot[rows] = np.arange(n, dtype=np.uint32)
+    cap = int(out_deg[rows].astype(np.uint64).sum())
+    off = aligned_empty(n + 1, np.uint64)
+    nbr = aligned_empty(cap, np.uint32)
+    rc = _L().hytgen_rmat_rows(c["scale"], c["V"], c["E"], *c["abc"], c["seed"], int(c["symmetric"]),
+                               _p(slot), n, _p(off), _p(nbr), cap)
+    if rc != 0:
+        raise ValueError(f"hytgen_rmat_rows rc={rc}")
+    w = None
+    if weighted:
+        w = aligned_empty(cap, np.uint32)
+        _L().hytgen_weights_rows(n, _p(rows), _p(off), _p(nbr), c["seed"] + 1000, _p(w))
+    return off, nbr, w

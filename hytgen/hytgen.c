@@ -219,6 +219,128 @@ int hytgen_rmat_csr(int scale, uint64_t V, uint64_t E, double a, double b, doubl
     return 0;
 }
 
+/* ---------------- per-rank (shard) generation, SURVEY §7.2 #6 ----------------
+ * A multi-GPU job never materialises the whole graph in one process.  Every
+ * edge is a pure function of its index (counter-based draws), so a rank can
+ *   1. count the degrees of an edge-index range [e0, e1) (each rank one slice;
+ *      the caller sums the slices across ranks: O(V) per rank), and
+ *   2. build the rows of ANY vertex subset by regenerating every edge and
+ *      keeping those whose source is in the subset (O(E) draws, O(own edges)
+ *      memory).  slot[v] = the local row of v, or 0xFFFFFFFF if v is not kept;
+ *      rows come out in local-row order, each sorted ascending, identical to
+ *      the same rows of hytgen_rmat_csr's full CSR.                            */
+
+typedef struct {
+    const rmat_params *p;
+    uint64_t e0, e1;
+    int symmetric;
+    uint32_t *out_deg, *in_deg;
+} deg_job;
+
+static void *deg_worker(void *arg) {
+    deg_job *j = (deg_job *)arg;
+    for (uint64_t e = j->e0; e < j->e1; ++e) {
+        uint32_t u, v;
+        rmat_edge(j->p, e, &u, &v);
+        __atomic_fetch_add(&j->out_deg[u], 1u, __ATOMIC_RELAXED);
+        __atomic_fetch_add(&j->in_deg[v], 1u, __ATOMIC_RELAXED);
+        if (j->symmetric) {
+            __atomic_fetch_add(&j->out_deg[v], 1u, __ATOMIC_RELAXED);
+            __atomic_fetch_add(&j->in_deg[u], 1u, __ATOMIC_RELAXED);
+        }
+    }
+    return NULL;
+}
+
+/* Adds the stored out-/in-degrees of edges [e0, e1) into out_deg / in_deg (u32[V]). */
+int hytgen_rmat_degrees(int scale, uint64_t V, uint64_t E, double a, double b, double c, uint64_t seed,
+                        int symmetric, uint64_t e0, uint64_t e1, uint32_t *out_deg, uint32_t *in_deg) {
+    if (scale < 1 || scale > 32 || V == 0 || V > (1ull << scale) || e0 > e1 || e1 > E) return -1;
+    rmat_params p; make_params(&p, scale, V, E, a, b, c, seed);
+    int nt = hytgen_num_threads();
+    pthread_t th[256]; deg_job jobs[256];
+    for (int t = 0; t < nt; ++t) {
+        jobs[t].p = &p; jobs[t].symmetric = symmetric; jobs[t].out_deg = out_deg; jobs[t].in_deg = in_deg;
+        jobs[t].e0 = e0 + (e1 - e0) * t / nt; jobs[t].e1 = e0 + (e1 - e0) * (t + 1) / nt;
+        pthread_create(&th[t], NULL, deg_worker, &jobs[t]);
+    }
+    for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+    return 0;
+}
+
+typedef struct {
+    const rmat_params *p;
+    uint64_t e0, e1;
+    int symmetric, pass;
+    const uint32_t *slot;
+    uint32_t *cnt;      /* pass 1 */
+    uint64_t *cursor;   /* pass 2 */
+    uint32_t *nbr;
+} rows_job;
+
+static void *rows_worker(void *arg) {
+    rows_job *j = (rows_job *)arg;
+    for (uint64_t e = j->e0; e < j->e1; ++e) {
+        uint32_t u, v;
+        rmat_edge(j->p, e, &u, &v);
+        for (int dir = 0; dir < 1 + j->symmetric; ++dir) {
+            uint32_t s = dir ? v : u, d = dir ? u : v;
+            uint32_t r = j->slot[s];
+            if (r == 0xFFFFFFFFu) continue;
+            if (j->pass == 1) __atomic_fetch_add(&j->cnt[r], 1u, __ATOMIC_RELAXED);
+            else j->nbr[__atomic_fetch_add(&j->cursor[r], 1ull, __ATOMIC_RELAXED)] = d;
+        }
+    }
+    return NULL;
+}
+
+/* Rows of the kept vertices: off_local u64[nrows+1]; nbr_local sized by the
+ * caller from the global out-degrees (sum over kept vertices), checked here.
+ * Returns 0, -1 (bad args), -2 (no memory), -3 (edge count != cap). */
+int hytgen_rmat_rows(int scale, uint64_t V, uint64_t E, double a, double b, double c, uint64_t seed,
+                     int symmetric, const uint32_t *slot, uint64_t nrows, uint64_t *off_local,
+                     uint32_t *nbr_local, uint64_t cap) {
+    if (scale < 1 || scale > 32 || V == 0 || V > (1ull << scale)) return -1;
+    rmat_params p; make_params(&p, scale, V, E, a, b, c, seed);
+    int nt = hytgen_num_threads();
+    uint32_t *cnt = (uint32_t *)calloc(nrows ? nrows : 1, sizeof(uint32_t));
+    uint64_t *cursor = (uint64_t *)malloc((nrows ? nrows : 1) * sizeof(uint64_t));
+    if (!cnt || !cursor) { free(cnt); free(cursor); return -2; }
+    pthread_t th[256]; rows_job jobs[256];
+    for (int pass = 1; pass <= 2; ++pass) {
+        if (pass == 2) {
+            off_local[0] = 0;
+            for (uint64_t r = 0; r < nrows; ++r) off_local[r + 1] = off_local[r] + cnt[r];
+            if (off_local[nrows] != cap) { free(cnt); free(cursor); return -3; }
+            memcpy(cursor, off_local, nrows * sizeof(uint64_t));
+        }
+        for (int t = 0; t < nt; ++t) {
+            jobs[t].p = &p; jobs[t].symmetric = symmetric; jobs[t].pass = pass; jobs[t].slot = slot;
+            jobs[t].cnt = cnt; jobs[t].cursor = cursor; jobs[t].nbr = nbr_local;
+            jobs[t].e0 = E * t / nt; jobs[t].e1 = E * (t + 1) / nt;
+            pthread_create(&th[t], NULL, rows_worker, &jobs[t]);
+        }
+        for (int t = 0; t < nt; ++t) pthread_join(th[t], NULL);
+    }
+    free(cnt); free(cursor);
+    sort_rows(off_local, nbr_local, nrows, nt);
+    return 0;
+}
+
+/* Weights of local rows: rows[r] = the original id of local row r. */
+int hytgen_weights_rows(uint64_t nrows, const uint32_t *rows, const uint64_t *off_local, const uint32_t *nbr,
+                        uint64_t seed, uint32_t *w) {
+    for (uint64_t r = 0; r < nrows; ++r) {
+        uint64_t u = rows[r];
+        for (uint64_t k = off_local[r]; k < off_local[r + 1]; ++k) {
+            uint64_t v = nbr[k];
+            uint64_t lo = u < v ? u : v, hi = u < v ? v : u;
+            w[k] = 1u + (uint32_t)(splitmix64(seed ^ ((lo << 32) | hi)) % 63u);
+        }
+    }
+    return 0;
+}
+
 /* Build a CSR from an explicit edge list (tests, crafted graphs). Rows sorted. */
 int hytgen_csr_from_edges(uint64_t V, uint64_t M, const uint32_t *src, const uint32_t *dst,
                           int symmetric, uint64_t *off, uint32_t *nbr) {

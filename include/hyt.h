@@ -58,6 +58,15 @@ extern "C" {
 #define HYT_SYMMETRIC  2u /* the caller asserts the edge set is symmetric (every    */
                           /* (u,v) has (v,u), e.g. a symmetrised undirected graph): */
                           /* enables pull iterations for BFS / CC (param direction) */
+#define HYT_ADOPT_HOST 4u /* with HYT_NO_HUBSORT: the caller's u32 id array IS the  */
+                          /* edge store (the paper keeps edges in host memory,      */
+                          /* P:75): it is page-locked and mapped in place,   */
+                          /* not copied, so host memory holds one copy of the ids.  */
+                          /* The caller keeps it alive and unmodified until         */
+                          /* hyt_free.  Needs a 16-byte aligned array whose first   */
+                          /* element is on a 16-byte chunk of the global edge order */
+                          /* (always true for world 1).  SSSP's packed (id, weight) */
+                          /* records are still built in library memory.             */
 
 /* ---- engine modes (hyt_set_param "engine_mode") ---- */
 #define HYT_MODE_HYBRID     0  /* the paper: per-partition cost-model selection    */
@@ -119,6 +128,8 @@ typedef struct {
     /* device bytes withheld from the driver so managed pages fit the budget     */
     uint64_t pull_iters, um_balloon_bytes;
     uint64_t exch_peer;            /* iterations exchanged by fused peer push (exchange = 3) */
+    uint64_t host_store_bytes;     /* pinned host bytes the library owns for this rank's  */
+                                   /* edge store (0 for adopted ids, HYT_ADOPT_HOST)      */
 } hyt_stats;
 
 /* One row per iteration (hyt_get_iter_log), the Fig. 7 / Table VI analog. */
@@ -168,6 +179,33 @@ int hyt_set_device_arena(hyt_graph *g, void *dptr, uint64_t bytes);
  * HYT_ENOMEM (pinning or budget), HYT_ECUDA, HYT_ESTATE (already loaded). */
 int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host,
                  const uint32_t *nbr_host, const uint32_t *w_host, uint32_t flags);
+
+/* ---- two-phase (shard) load: no process holds the whole graph ----
+ * For graphs larger than one host's memory per rank (BASELINE configs[4], RMAT-30
+ * over 8 ranks): every rank passes only O(V) global data plus the rows it
+ * serves.
+ *   1. hyt_load_shard_begin: out_deg_host / in_deg_host are the GLOBAL out- and
+ *      in-degrees, u32[V] each, by caller id (e.g. each rank counts a slice of
+ *      the edges and the ranks sum them).  The library hub-sorts
+ *      exactly as hyt_load_csr would (same permutation on every rank) and
+ *      returns this rank's internal vertex range [*row_lo, *row_hi) (the split
+ *      of hyt_rank_range) and its edge count *edges.
+ *   2. hyt_get_shard_rows: rows_host[i] = the caller id of internal row
+ *      row_lo + i (u32[n], n = row_hi - row_lo).
+ *   3. hyt_load_shard_rows: the caller passes exactly those rows in that order
+ *      as a local CSR: row_off_host u64[nrows+1] (row_off[0] = 0, row_off[nrows]
+ *      = *edges), nbr_host u32[*edges] with CALLER neighbour ids, optional
+ *      w_host u32[*edges].  Each row's length must equal its out-degree.  The
+ *      library relabels them on the GPU into its pinned store (or adopts the id
+ *      array with HYT_ADOPT_HOST).
+ * Flags as hyt_load_csr, given to begin.  After step 3 the handle is loaded and
+ * everything else is unchanged.  Errors: HYT_EINVAL (degree sums differ, a row
+ * length or id out of range), HYT_ESTATE (out of order), HYT_ENOMEM. */
+int hyt_load_shard_begin(hyt_graph *g, uint64_t V, const uint32_t *out_deg_host, const uint32_t *in_deg_host,
+                         uint32_t flags, uint64_t *row_lo, uint64_t *row_hi, uint64_t *edges);
+int hyt_get_shard_rows(hyt_graph *g, uint32_t *rows_host, uint64_t n);
+int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off_host, const uint32_t *nbr_host,
+                        const uint32_t *w_host);
 
 /* Set a run parameter.  Keys (defaults in brackets):
  *   alpha [0.8], beta [0.4]; gamma [0.625]; m [128],

@@ -32,6 +32,7 @@ HYT_BFS, HYT_SSSP, HYT_CC, HYT_PR = 0, 1, 2, 3
 ALGOS = {"bfs": HYT_BFS, "sssp": HYT_SSSP, "cc": HYT_CC, "pr": HYT_PR}
 HYT_NO_HUBSORT = 1
 HYT_SYMMETRIC = 2
+HYT_ADOPT_HOST = 4
 MODES = {"hybrid": 0, "filter": 1, "compaction": 2, "zerocopy": 3, "resident": 4, "um": 5}
 HYT_ENG_NONE, HYT_ENG_F, HYT_ENG_C, HYT_ENG_Z, HYT_ENG_R = 0, 1, 2, 3, 4
 TAGS = ["plan", "filter", "compaction", "zerocopy", "resident", "recompute", "copy", "recompute_queue"]
@@ -49,7 +50,7 @@ class hyt_stats(ctypes.Structure):
         ("cal_link_gbs", ctypes.c_double), ("cal_cpt_gbs", ctypes.c_double), ("cal_zc_req_ns", ctypes.c_double),
         ("cal_zc_line_ns", ctypes.c_double), ("exch_sparse", ctypes.c_uint64), ("exch_dense", ctypes.c_uint64),
         ("exch_bytes", ctypes.c_uint64), ("pull_iters", ctypes.c_uint64), ("um_balloon_bytes", ctypes.c_uint64),
-        ("exch_peer", ctypes.c_uint64)]
+        ("exch_peer", ctypes.c_uint64), ("host_store_bytes", ctypes.c_uint64)]
 
 
 class hyt_iter(ctypes.Structure):
@@ -66,6 +67,10 @@ _SIGS = {
     "hyt_set_device_budget": ([_vp, _u64], _i32),
     "hyt_set_device_arena": ([_vp, _vp, _u64], _i32),
     "hyt_load_csr": ([_vp, _u64, _u64, _vp, _vp, _vp, _u32], _i32),
+    "hyt_load_shard_begin": ([_vp, _u64, _vp, _vp, _u32, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
+                              ctypes.POINTER(_u64)], _i32),
+    "hyt_get_shard_rows": ([_vp, _vp, _u64], _i32),
+    "hyt_load_shard_rows": ([_vp, _u64, _vp, _vp, _vp], _i32),
     "hyt_set_param": ([_vp, ctypes.c_char_p, ctypes.c_double], _i32),
     "hyt_run": ([_vp, _i32, _u64], _i32),
     "hyt_get_values": ([_vp, _vp, _u64], _i32),
@@ -153,17 +158,53 @@ class Graph:
         """Join an in-process group (one thread per rank; testing the multi-rank path on one GPU)."""
         check(hyt_init_dist_local(self.h, rank, world, group), "hyt_init_dist_local")
 
-    def load(self, off, nbr, w=None, hubsort: bool = True, symmetric: bool = False) -> None:
+    @staticmethod
+    def _flags(hubsort: bool, symmetric: bool, adopt: bool) -> int:
+        return ((0 if hubsort else HYT_NO_HUBSORT) | (HYT_SYMMETRIC if symmetric else 0) |
+                (HYT_ADOPT_HOST if adopt else 0))
+
+    def load(self, off, nbr, w=None, hubsort: bool = True, symmetric: bool = False, adopt: bool = False) -> None:
         off = np.ascontiguousarray(off, dtype=np.uint64)
         nbr = np.ascontiguousarray(nbr, dtype=np.uint32)
         if w is not None:
             w = np.ascontiguousarray(w, dtype=np.uint32)
         V = len(off) - 1
         E = int(off[-1]) if V >= 0 else 0
+        if adopt:
+            self._adopted = nbr             # the library reads it until close()
         check(hyt_load_csr(self.h, V, E, _ptr(off), _ptr(nbr) if E else None, _ptr(w) if w is not None else None,
-                           (0 if hubsort else HYT_NO_HUBSORT) | (HYT_SYMMETRIC if symmetric else 0)),
-              "hyt_load_csr")
+                           self._flags(hubsort, symmetric, adopt)), "hyt_load_csr")
         self.V = V
+
+    def load_shard_begin(self, out_deg, in_deg, hubsort: bool = True, symmetric: bool = False,
+                         adopt: bool = False) -> dict:
+        """Two-phase load, step 1 (include/hyt.h): global u32[V] out-/in-degrees by
+        caller id -> this rank's internal row range and edge count."""
+        out_deg = np.ascontiguousarray(out_deg, dtype=np.uint32)
+        in_deg = np.ascontiguousarray(in_deg, dtype=np.uint32)
+        lo, hi, ne = _u64(), _u64(), _u64()
+        check(hyt_load_shard_begin(self.h, len(out_deg), _ptr(out_deg), _ptr(in_deg),
+                                   self._flags(hubsort, symmetric, adopt), ctypes.byref(lo), ctypes.byref(hi),
+                                   ctypes.byref(ne)), "hyt_load_shard_begin")
+        self.V = len(out_deg)
+        return {"row_lo": lo.value, "row_hi": hi.value, "edges": ne.value}
+
+    def shard_rows(self, n: int) -> np.ndarray:
+        """Step 2: caller ids of this rank's internal rows, in internal order."""
+        out = np.empty(n, dtype=np.uint32)
+        check(hyt_get_shard_rows(self.h, _ptr(out) if n else None, n), "hyt_get_shard_rows")
+        return out
+
+    def load_shard_rows(self, row_off, nbr, w=None, adopt: bool = False) -> None:
+        """Step 3: those rows as a local CSR (caller neighbour ids)."""
+        row_off = np.ascontiguousarray(row_off, dtype=np.uint64)
+        nbr = np.ascontiguousarray(nbr, dtype=np.uint32)
+        if w is not None:
+            w = np.ascontiguousarray(w, dtype=np.uint32)
+        if adopt:
+            self._adopted = nbr
+        check(hyt_load_shard_rows(self.h, len(row_off) - 1, _ptr(row_off), _ptr(nbr) if len(nbr) else None,
+                                  _ptr(w) if w is not None else None), "hyt_load_shard_rows")
 
     def run(self, algo, source: int = 0) -> None:
         a = ALGOS[algo] if isinstance(algo, str) else int(algo)
@@ -219,6 +260,7 @@ class Graph:
             hyt_free(self.h)
             self.h = None
         self._arena_tensor = None
+        self._adopted = None
 
     def __del__(self):
         try:

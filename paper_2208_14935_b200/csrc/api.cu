@@ -72,8 +72,32 @@ int hyt_load_csr(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, cons
                  const uint32_t *w, uint32_t flags) {
     HYT_GUARD({
         HYT_REQUIRE(g, HYT_EINVAL, "null handle");
-        HYT_REQUIRE((flags & ~(HYT_NO_HUBSORT | HYT_SYMMETRIC)) == 0, HYT_EINVAL, "unknown flags");
+        HYT_REQUIRE((flags & ~(HYT_NO_HUBSORT | HYT_SYMMETRIC | HYT_ADOPT_HOST)) == 0, HYT_EINVAL, "unknown flags");
         load_graph(g, V, E, off, nbr, w, flags);
+    })
+}
+
+int hyt_load_shard_begin(hyt_graph *g, uint64_t V, const uint32_t *out_deg, const uint32_t *in_deg, uint32_t flags,
+                         uint64_t *row_lo, uint64_t *row_hi, uint64_t *edges) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && row_lo && row_hi && edges, HYT_EINVAL, "null argument");
+        HYT_REQUIRE((flags & ~(HYT_NO_HUBSORT | HYT_SYMMETRIC | HYT_ADOPT_HOST)) == 0, HYT_EINVAL, "unknown flags");
+        load_shard_begin(g, V, out_deg, in_deg, flags, row_lo, row_hi, edges);
+    })
+}
+
+int hyt_get_shard_rows(hyt_graph *g, uint32_t *rows, uint64_t n) {
+    HYT_GUARD({
+        HYT_REQUIRE(g && (rows || n == 0), HYT_EINVAL, "null argument");
+        shard_rows(g, rows, n);
+    })
+}
+
+int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off, const uint32_t *nbr,
+                        const uint32_t *w) {
+    HYT_GUARD({
+        HYT_REQUIRE(g, HYT_EINVAL, "null handle");
+        load_shard_rows(g, nrows, row_off, nbr, w);
     })
 }
 
@@ -94,7 +118,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "d2") { integral(); in(0, 64); p.d2 = (uint64_t)v; }
         else if (k == "k") { integral(); in(1, 1024); p.k = (uint64_t)v; }
         else if (k == "partition_bytes") { integral(); in(16, 1e12); p.partition_bytes = (uint64_t)v; }
-        else if (k == "hub_fraction") { in(0, 1); HYT_REQUIRE(!g->loaded, HYT_ESTATE, "hub_fraction applies at load"); p.hub_fraction = v; }
+        else if (k == "hub_fraction") { in(0, 1); HYT_REQUIRE(!g->loaded && !g->planned, HYT_ESTATE, "hub_fraction applies at load"); p.hub_fraction = v; }
         else if (k == "streams") { integral(); in(1, 8); p.streams = (int)v; }
         else if (k == "engine_mode") { integral(); in(0, 5); p.engine_mode = (int)v; }
         else if (k == "priority") { integral(); in(-1, 2); p.priority = (int)v; }

@@ -1292,6 +1292,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     g->stats.cal_cpt_gbs = g->est_cpt_gbs;
     g->stats.cal_zc_req_ns = g->est_zc_req_ns;
     g->stats.cal_zc_line_ns = g->est_zc_line_ns;
+    g->stats.host_store_bytes = g->store_bytes;
     for (int i = 0; i < 8; ++i) { g->stats.eng_ms[i] = 0; g->stats.eng_launches[i] = 0; g->stats.eng_chunks[i] = 0; g->stats.eng_edges[i] = 0; }
     g->stats.eng_ms[0] = g->plan_time.ms; g->stats.eng_launches[0] = g->plan_time.launches;
     for (int i = 1; i < ENG_COUNT; ++i) {
@@ -1386,6 +1387,7 @@ void free_graph(hyt_graph *g) {
     release_run_ctx(g);
     for (auto s : g->st) cudaStreamDestroy(s);
     if (g->main) cudaStreamDestroy(g->main);
+    release_adopted(g);
     pinned_free(g->nbr_h);
     pinned_free(g->ew_h);
     dist_free(g);

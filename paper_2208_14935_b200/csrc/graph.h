@@ -138,6 +138,13 @@ struct hyt_graph {
     uint32_t *new_id_d = nullptr;   // caller id -> internal id
     uint32_t *old_of_d = nullptr;   // internal id -> caller id
     uint32_t *din_d = nullptr;      // in-degree (internal ids)
+    uint64_t store_bytes = 0;       // pinned host bytes this handle owns for its edge store
+    bool nbr_adopted = false;       // HYT_ADOPT_HOST: nbr_h is the caller's (registered) array
+    const void *adopt_key = nullptr, *adopt_dev = nullptr;
+    // ---- two-phase (shard) load state ----
+    bool planned = false;           // hyt_load_shard_begin done, rows not yet loaded
+    uint32_t ld_flags = 0;
+    uint64_t *ld_off_old = nullptr; // device: caller offsets (original order), until the rows are loaded
     // ---- streams ----
     cudaStream_t main = nullptr;
     std::vector<cudaStream_t> st;   // worker streams
@@ -167,6 +174,11 @@ struct hyt_graph {
 namespace hyt {
 void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const uint32_t *nbr,
                 const uint32_t *w, uint32_t flags);
+void load_shard_begin(hyt_graph *g, uint64_t V, const uint32_t *out_deg, const uint32_t *in_deg, uint32_t flags,
+                      uint64_t *row_lo, uint64_t *row_hi, uint64_t *edges);
+void shard_rows(hyt_graph *g, uint32_t *rows, uint64_t n);
+void load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off, const uint32_t *nbr, const uint32_t *w);
+void release_adopted(hyt_graph *g);
 void run_graph(hyt_graph *g, int algo, uint64_t source);
 void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_parts, uint64_t *bounds,
                 uint64_t *t, uint64_t *e, uint64_t *a, uint64_t *z, uint8_t *p);

@@ -3,7 +3,6 @@
 // (the paper's storage split: vertex data on the GPU, edges in host memory,
 // P:75).  All per-vertex and per-edge work runs on the GPU; the
 // caller's edge arrays are read in place through a temporary host mapping.
-#include <cub/cub.cuh>
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -14,6 +13,8 @@
 #include <thread>
 #include <unordered_map>
 #include "graph.h"
+#include "scan.h"
+#include "block_prims.cuh"
 
 namespace hyt {
 
@@ -175,12 +176,17 @@ __global__ void k_finish_perm(uint64_t V, uint64_t h, const uint32_t *__restrict
 // are both coalesced (consecutive slots of a row are consecutive on both sides).
 constexpr int kRelabelTile = 8192, kRelabelRows = 2048;
 
+// row_start (shard loads): the first edge of internal row r in the caller's local
+// arrays is row_start[r - r_base] (rows r_base..r_end-1 only); otherwise it is
+// off_old[old_of[r]] in the caller's full arrays.  A neighbour id >= V sets *bad.
+// nbr_out may be null (HYT_ADOPT_HOST: the caller's ids are the store).
 __global__ void __launch_bounds__(512)
 k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__restrict__ off_old,
                 const uint64_t *__restrict__ off_new,
                 const uint32_t *__restrict__ old_of, const uint32_t *__restrict__ new_id,
+                const uint64_t *__restrict__ row_start, uint64_t r_base, uint64_t r_end,
                 const uint32_t *__restrict__ nbr_in, const uint32_t *__restrict__ w_in,
-                uint32_t *__restrict__ nbr_out, uint64_t *__restrict__ ew_out) {
+                uint32_t *__restrict__ nbr_out, uint64_t *__restrict__ ew_out, uint32_t *__restrict__ bad) {
     __shared__ uint64_t s_new[kRelabelRows + 1];
     __shared__ uint64_t s_old[kRelabelRows];
     __shared__ uint64_t s_r0;
@@ -205,7 +211,11 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
             const uint64_t nr = min((uint64_t)kRelabelRows, V - r0);
             for (uint64_t i = threadIdx.x; i <= nr; i += blockDim.x) {
                 s_new[i] = off_new[r0 + i];
-                if (i < nr) s_old[i] = off_old[old_of[r0 + i]];
+                if (i < nr) {
+                    const uint64_t r = r0 + i;
+                    s_old[i] = row_start ? ((r >= r_base && r < r_end) ? row_start[r - r_base] : 0)
+                                         : off_old[old_of[r]];
+                }
             }
             __syncthreads();
             const uint64_t stop = min(e_end, s_new[nr]);   // edges the staged rows cover
@@ -216,13 +226,29 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
                     if (s_new[mid] <= x) lo = mid; else hi = mid - 1;
                 }
                 const uint64_t src = s_old[lo] + (x - s_new[lo]);
-                const uint32_t y = new_id[nbr_in[src]];
-                nbr_out[x] = y;
+                const uint32_t id = nbr_in[src];
+                if (id >= V) { *bad = 1; continue; }
+                const uint32_t y = new_id[id];
+                if (nbr_out) nbr_out[x] = y;
                 if (ew_out) ew_out[x] = (uint64_t)y | ((uint64_t)w_in[src] << 32);
             }
             e = stop;
         }
     }
+}
+
+__global__ void k_u32_to_u64(const uint32_t *__restrict__ in, uint64_t n, uint64_t *__restrict__ out) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = in[i];
+}
+
+__global__ void k_sum_u32(const uint32_t *__restrict__ in, uint64_t n, unsigned long long *__restrict__ sum) {
+    __shared__ uint64_t sh[33];
+    uint64_t s = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) s += in[i];
+    s = block_sum_u64(s, sh);
+    if (threadIdx.x == 0 && s) atomicAdd(sum, (unsigned long long)s);
 }
 
 // ---------------------------------------------------------------------------
@@ -313,75 +339,276 @@ struct HostView {
 };
 
 // ---------------------------------------------------------------------------
-// load
+// load, in two phases.
+//   plan: validate the degrees, hub-sort on the GPU, build the new
+//         offsets and this rank's vertex range.  Needs only O(V) data: the
+//         caller's offsets (or out-degrees) and in-degrees (computed from the
+//         caller's edges when not given).
+//   rows: pin this rank's edge store and write the relabelled rows into it,
+//         reading the caller's rows in place through a host mapping: either the
+//         whole CSR (hyt_load_csr) or only the rows of this rank's range in
+//         internal order (hyt_load_shard_rows: no process holds the whole graph).
 // ---------------------------------------------------------------------------
 static double wall_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
-void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const uint32_t *nbr,
-                const uint32_t *w, uint32_t flags) {
-    const bool verbose = getenv("HYT_VERBOSE") != nullptr;
-    double tph = wall_ms();
-    auto phase = [&](const char *name) {
+struct Phase {
+    hyt_graph *g;
+    bool verbose = getenv("HYT_VERBOSE") != nullptr;
+    double t = wall_ms();
+    void operator()(const char *name) {
         if (!verbose) return;
         cudaStreamSynchronize(g->main);
-        const double t = wall_ms();
-        fprintf(stderr, "[hyt load] %-28s %8.1f ms\n", name, t - tph);
-        tph = t;
-    };
-    HYT_REQUIRE(!g->loaded, HYT_ESTATE, "graph already loaded");
-    HYT_REQUIRE(V > 0 && V < (1ull << 32), HYT_EINVAL, "V must be in [1, 2^32)");
-    HYT_REQUIRE(off != nullptr && (E == 0 || nbr != nullptr), HYT_EINVAL, "null CSR array");
-    HYT_REQUIRE(off[0] == 0, HYT_EINVAL, "off[0] != 0");
-    HYT_REQUIRE(off[V] == E, HYT_EINVAL, "off[V] != E");
-    for (uint64_t v = 0; v < V; ++v)
-        HYT_REQUIRE(off[v] <= off[v + 1], HYT_EINVAL, "offsets not non-decreasing at " + std::to_string(v));
-    HYT_CUDA(cudaSetDevice(g->device));
+        const double n = wall_ms();
+        fprintf(stderr, "[hyt load] %-28s %8.1f ms\n", name, n - t);
+        t = n;
+    }
+};
+
+// Pinning the store on a host thread while the GPU computes the hub sort (one
+// rank owns every edge, so the store's size is known before the plan).
+struct EarlyStore {
+    std::thread th;
+    void *n = nullptr, *w = nullptr;
+    uint64_t nbytes = 0, wbytes = 0;
+    std::exception_ptr err;
+    ~EarlyStore() {
+        if (th.joinable()) th.join();
+        pinned_free(n);
+        pinned_free(w);
+    }
+};
+
+struct Temps {   // arena temporaries, released in reverse order
+    Arena &A;
+    std::vector<void *> v;
+    explicit Temps(Arena &a) : A(a) {}
+    void *get(uint64_t bytes, const char *what) { void *p = A.alloc(bytes, what); v.push_back(p); return p; }
+    void drop(void *p) {
+        A.release(p);
+        v.erase(std::find(v.begin(), v.end(), p));
+    }
+    ~Temps() { for (auto it = v.rbegin(); it != v.rend(); ++it) A.release(*it); }
+};
+
+static uint32_t read_flag(uint32_t *bad, cudaStream_t st) {
+    uint32_t h = 0;
+    HYT_CUDA(copy_sync(&h, bad, 4, st));
+    return h;
+}
+
+// off_host: caller offsets u64[V+1] (full CSR), or out_deg u32[V] (shard);
+// in_deg u32[V] or null (then nbr_dev, the caller's full ids mapped, is counted).
+static void plan_phase(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host, const uint32_t *out_deg,
+                       const uint32_t *in_deg, const uint32_t *nbr_dev, uint32_t flags, Phase &phase) {
     Arena &A = g->arena;
     cudaStream_t st = g->main;
-    g->V = V; g->E = E; g->weighted = (w != nullptr); g->symmetric = (flags & HYT_SYMMETRIC) != 0;
-
-    // persistent device arrays
+    g->V = V; g->E = E; g->symmetric = (flags & HYT_SYMMETRIC) != 0;
     g->off_d = arena_new<uint64_t>(A, V + 1, "offsets");
     g->new_id_d = arena_new<uint32_t>(A, V, "new_id");
     g->old_of_d = arena_new<uint32_t>(A, V, "old_of");
     g->din_d = arena_new<uint32_t>(A, V, "in_degree");
-
-    // temporaries (released in reverse order)
-    std::vector<void *> tmp;
-    auto T = [&](uint64_t bytes, const char *what) { void *p = A.alloc(bytes, what); tmp.push_back(p); return p; };
-    uint64_t *off_old = (uint64_t *)T((V + 1) * 8, "load: caller offsets");
-    uint32_t *din = (uint32_t *)T(V * 4 + 16, "load: in-degree");
-    uint32_t *bad = (uint32_t *)T(16, "load: flag");
-    uint32_t *nonhub = (uint32_t *)T(V * 4 + 16, "load: non-hub flags");
-    uint32_t *nonhub_scan = (uint32_t *)T(V * 4 + 16, "load: non-hub scan");
-    HYT_CUDA(cudaMemcpyAsync(off_old, off, (V + 1) * 8, cudaMemcpyHostToDevice, st));
-    HYT_CUDA(cudaMemsetAsync(din, 0, V * 4, st));
+    // caller offsets: kept until the rows are loaded (the full-CSR relabel reads them)
+    g->ld_off_old = arena_new<uint64_t>(A, V + 1, "load: caller offsets");
+    uint64_t *off_old = g->ld_off_old;
+    Temps T(A);
+    uint32_t *din = (uint32_t *)T.get(V * 4 + 16, "load: in-degree");
+    uint32_t *bad = (uint32_t *)T.get(16, "load: flag");
+    uint32_t *nonhub = (uint32_t *)T.get(V * 4 + 16, "load: non-hub flags");
+    uint32_t *nonhub_scan = (uint32_t *)T.get(V * 4 + 16, "load: non-hub scan");
+    void *stemp = T.get(scan_temp_bytes(V + 1) + 16, "load: scan temp");
     HYT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+    if (off_host) {
+        HYT_CUDA(cudaMemcpyAsync(off_old, off_host, (V + 1) * 8, cudaMemcpyHostToDevice, st));
+    } else {   // offsets = exclusive scan of the out-degrees (V+1 items, the last 0)
+        uint32_t *od = (uint32_t *)T.get((V + 1) * 4 + 16, "load: out-degrees");
+        HYT_CUDA(cudaMemcpyAsync(od, out_deg, V * 4, cudaMemcpyHostToDevice, st));
+        HYT_CUDA(cudaMemsetAsync(od + V, 0, 4, st));
+        exclusive_scan<uint32_t, uint64_t>(od, off_old, V + 1, stemp, st);
+        HYT_CUDA(copy_sync(&E, off_old + V, 8, st));
+        g->E = E;
+        T.drop(od);
+    }
+    if (in_deg) {
+        HYT_CUDA(cudaMemcpyAsync(din, in_deg, V * 4, cudaMemcpyHostToDevice, st));
+        unsigned long long *sum = (unsigned long long *)T.get(16, "load: in-degree sum");
+        HYT_CUDA(cudaMemsetAsync(sum, 0, 8, st));
+        k_sum_u32<<<grid_for(V, 256, num_sms() * 8), 256, 0, st>>>(din, V, sum);
+        unsigned long long se = 0;
+        HYT_CUDA(copy_sync(&se, sum, 8, st));
+        HYT_REQUIRE(se == E, HYT_EINVAL, "sum of in-degrees != sum of out-degrees");
+        T.drop(sum);
+    } else {
+        HYT_CUDA(cudaMemsetAsync(din, 0, V * 4, st));
+        if (E) k_indeg<<<grid_for(E), 256, 0, st>>>(nbr_dev, E, V, din, bad);
+        HYT_REQUIRE(read_flag(bad, st) == 0, HYT_EINVAL, "neighbour id >= V");
+    }
+    if (flags & HYT_SYMMETRIC) {
+        k_sym_degrees<<<grid_for(V), 256, 0, st>>>(off_old, din, V, bad);
+        HYT_REQUIRE(read_flag(bad, st) == 0, HYT_EINVAL,
+                    "HYT_SYMMETRIC: some vertex's in-degree differs from its out-degree");
+    }
+    phase("degrees");
 
-    phase("validate + device alloc");
-    // One rank owns every edge, so the store's size is known now: pin it on a host
-    // thread while the GPU computes in-degrees and the hub sort.
-    struct EarlyStore {
-        std::thread th;
-        void *n = nullptr, *w = nullptr;
-        std::exception_ptr err;
-        ~EarlyStore() {
-            if (th.joinable()) th.join();
-            pinned_free(n);
-            pinned_free(w);
+    // ---- hub sort: top h = ceil(frac*V) by D_o*D_i ----
+    const uint64_t fden = 1000000;
+    const uint64_t fnum = (uint64_t)(g->prm.hub_fraction * (double)fden + 0.5);
+    uint64_t h = (flags & HYT_NO_HUBSORT) ? 0 : (fnum * V + fden - 1) / fden;
+    if (h > V) h = V;
+    k_fill_u32<<<grid_for(V), 256, 0, st>>>(nonhub, V, 1u);
+    if (h > 0) {
+        // exact radix select of the h-th largest key T (8 passes of 8 bits), then
+        // only the h hubs are sorted: O(V) memory instead of a full-V key sort
+        unsigned long long *hist = (unsigned long long *)T.get(256 * 8, "load: select histogram");
+        std::vector<unsigned long long> hh(256);
+        uint64_t prefix = 0, mask = 0, kk = h;
+        for (int pass = 0; pass < 8; ++pass) {
+            const int shift = 56 - 8 * pass;
+            HYT_CUDA(cudaMemsetAsync(hist, 0, 256 * 8, st));
+            k_key_hist<<<grid_for(V, 256, num_sms() * 8), 256, 0, st>>>(off_old, din, V, prefix, mask, shift, hist);
+            HYT_CUDA(copy_sync(hh.data(), hist, 256 * 8, st));
+            unsigned long long acc = 0;
+            int d = 255;
+            for (; d > 0; --d) {
+                if (acc + hh[d] >= kk) break;
+                acc += hh[d];
+            }
+            kk -= acc;
+            prefix |= (uint64_t)d << shift;
+            mask |= 0xFFull << shift;
         }
-    } early;
-    const uint64_t early_nbytes = ((E * 4 + 15) & ~15ull) + 32, early_wbytes = ((E * 8 + 15) & ~15ull) + 32;
+        const uint64_t Tkey = prefix, ties = kk;      // hubs: key > T, plus `ties` of key == T by id
+        k_tie_flags<<<grid_for(V), 256, 0, st>>>(off_old, din, V, Tkey, nonhub);
+        exclusive_scan<uint32_t, uint32_t>(nonhub, nonhub_scan, V, stemp, st);
+        k_hub_flags<<<grid_for(V), 256, 0, st>>>(off_old, din, V, Tkey, ties, nonhub_scan, nonhub);
+        exclusive_scan<uint32_t, uint32_t>(nonhub, nonhub_scan, V, stemp, st);
+        uint32_t *hid = (uint32_t *)T.get(h * 4 + 16, "load: hub ids");
+        uint32_t *hid2 = (uint32_t *)T.get(h * 4 + 16, "load: hub ids (scratch)");
+        uint64_t *hkey = (uint64_t *)T.get(h * 8 + 16, "load: hub keys");
+        uint64_t *hkey2 = (uint64_t *)T.get(h * 8 + 16, "load: hub keys (scratch)");
+        uint32_t *sflag = (uint32_t *)T.get(h * 4 + 16, "load: sort flags");
+        uint32_t *spos = (uint32_t *)T.get(h * 4 + 16, "load: sort positions");
+        unsigned long long *smax = (unsigned long long *)T.get(16, "load: sort max");
+        // hub ids in ascending id order, so the stable sort keeps ties by id (C11)
+        k_scatter_hubs<<<grid_for(V), 256, 0, st>>>(off_old, din, V, nonhub, nonhub_scan, hid, hkey);
+        sort_desc_stable(hkey, hid, hkey2, hid2, h, sflag, spos, stemp, smax, st);
+        k_fill_u32<<<grid_for(V), 256, 0, st>>>(nonhub, V, 1u);
+        k_mark_hubs<<<grid_for(h), 256, 0, st>>>(hid, h, g->new_id_d, nonhub);
+        HYT_CUDA(cudaStreamSynchronize(st));
+        for (void *q : {(void *)smax, (void *)spos, (void *)sflag, (void *)hkey2, (void *)hkey, (void *)hid2,
+                        (void *)hid, (void *)hist})
+            T.drop(q);
+    }
+    uint64_t *deg2 = (uint64_t *)T.get((V + 1) * 8, "load: degrees");
+    exclusive_scan<uint32_t, uint32_t>(nonhub, nonhub_scan, V, stemp, st);
+    k_finish_perm<<<grid_for(V), 256, 0, st>>>(V, h, nonhub, nonhub_scan, off_old, din, g->new_id_d,
+                                              g->old_of_d, deg2, g->din_d);
+    exclusive_scan<uint64_t, uint64_t>(deg2, g->off_d, V + 1, stemp, st);
+    g->off_h.resize(V + 1);
+    HYT_CUDA(copy_sync(g->off_h.data(), g->off_d, (V + 1) * 8, st));
+    HYT_REQUIRE(g->off_h[V] == E, HYT_ESTATE, "internal: permuted offsets do not sum to E");
+    rank_vertex_range(g->off_h, g->world, g->rank, &g->store_v_lo, &g->store_v_hi);
+    phase("hub sort + new offsets");
+}
+
+// The pinned mapped edge store of this rank's vertex range (the whole
+// graph at world 1), from a 16-byte chunk boundary, 16-B padded so chunk loads
+// never overrun.  row_start: null = full caller arrays (indexed by off_old),
+// else the device copy of the caller's local row offsets.  adopt_ids: the
+// caller's local id array IS the u32 store (HYT_ADOPT_HOST, no relabel).
+static void rows_phase(hyt_graph *g, const uint64_t *row_start, const uint32_t *nbr_dev, const uint32_t *w_dev,
+                       bool weighted, EarlyStore *early, const uint32_t *adopt_ids, Phase &phase) {
+    cudaStream_t st = g->main;
+    const uint64_t V = g->V;
+    g->weighted = weighted;
+    const uint64_t e_lo = g->off_h[g->store_v_lo], e_hi = g->off_h[g->store_v_hi];
+    g->store_c0[0] = e_lo / 4;                          // first chunk of u32 ids
+    g->store_c0[1] = e_lo / 2;                          // first chunk of u64 records
+    const uint64_t nbase = g->store_c0[0] * 4, wbase = g->store_c0[1] * 2;
+    const uint64_t nbytes = (((e_hi - nbase) * 4 + 15) & ~15ull) + 32;
+    const uint64_t wbytes = (((e_hi - wbase) * 8 + 15) & ~15ull) + 32;
+    if (adopt_ids) {
+        g->nbr_h = const_cast<uint32_t *>(adopt_ids);
+        g->nbr_adopted = true;
+    }
+    if (early && early->th.joinable()) {
+        early->th.join();
+        if (early->err) std::rethrow_exception(early->err);
+        HYT_REQUIRE((adopt_ids || nbytes == early->nbytes) && (!weighted || wbytes == early->wbytes), HYT_ESTATE,
+                    "edge store size mismatch");
+        if (!adopt_ids) { g->nbr_h = (uint32_t *)early->n; early->n = nullptr; }   // ownership moves
+        g->ew_h = (uint64_t *)early->w;
+        early->w = nullptr;
+    } else {
+        if (!adopt_ids) g->nbr_h = (uint32_t *)pinned_alloc(nbytes);   // zero-filled (padding included)
+        if (weighted) g->ew_h = (uint64_t *)pinned_alloc(wbytes);
+    }
+    g->store_bytes = (adopt_ids ? 0 : nbytes) + (weighted ? wbytes : 0);
+    uint32_t *nbr_out = nullptr;
+    uint64_t *ew_out = nullptr;
+    if (!adopt_ids) HYT_CUDA(cudaHostGetDevicePointer((void **)&nbr_out, g->nbr_h, 0));
+    if (weighted) HYT_CUDA(cudaHostGetDevicePointer((void **)&ew_out, g->ew_h, 0));
+    phase("pin edge store");
+    Temps T(g->arena);
+    uint32_t *bad = (uint32_t *)T.get(16, "load: flag");
+    HYT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
+    if (e_hi > e_lo && (nbr_out || ew_out || row_start)) {
+        k_relabel_tiles<<<num_sms() * 4, 512, 0, st>>>(V, e_lo, e_hi, g->ld_off_old, g->off_d, g->old_of_d, g->new_id_d,
+                                                      row_start, g->store_v_lo, g->store_v_hi, nbr_dev, w_dev,
+                                                      nbr_out ? nbr_out - nbase : nullptr,
+                                                      ew_out ? ew_out - wbase : nullptr, bad);
+    }
+    HYT_REQUIRE(read_flag(bad, st) == 0, HYT_EINVAL, "neighbour id >= V");
+    HYT_CUDA(cudaGetLastError());
+    phase("relabel edges (zero-copy)");
+}
+
+static void load_done(hyt_graph *g) {
+    g->arena.release(g->ld_off_old);
+    g->ld_off_old = nullptr;
+    g->planned = false;
+    g->loaded = true;
+}
+
+static void load_fail(hyt_graph *g) {
+    cudaStreamSynchronize(g->main);
+    if (g->ld_off_old) g->arena.release(g->ld_off_old);
+    g->ld_off_old = nullptr;
+    g->planned = false;
+}
+
+static void check_offsets(const uint64_t *off, uint64_t V, uint64_t E) {
+    HYT_REQUIRE(off[0] == 0, HYT_EINVAL, "off[0] != 0");
+    HYT_REQUIRE(off[V] == E, HYT_EINVAL, "off[V] != E");
+    for (uint64_t v = 0; v < V; ++v)
+        HYT_REQUIRE(off[v] <= off[v + 1], HYT_EINVAL, "offsets not non-decreasing at " + std::to_string(v));
+}
+
+void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const uint32_t *nbr,
+                const uint32_t *w, uint32_t flags) {
+    Phase phase{g};
+    HYT_REQUIRE(!g->loaded && !g->planned, HYT_ESTATE, "graph already loaded");
+    HYT_REQUIRE(V > 0 && V < (1ull << 32), HYT_EINVAL, "V must be in [1, 2^32)");
+    HYT_REQUIRE(off != nullptr && (E == 0 || nbr != nullptr), HYT_EINVAL, "null CSR array");
+    check_offsets(off, V, E);
+    const bool adopt = (flags & HYT_ADOPT_HOST) != 0;
+    HYT_REQUIRE(!adopt || (flags & HYT_NO_HUBSORT), HYT_EINVAL, "HYT_ADOPT_HOST needs HYT_NO_HUBSORT");
+    HYT_REQUIRE(!adopt || ((uintptr_t)nbr & 15) == 0, HYT_EINVAL, "HYT_ADOPT_HOST needs a 16-byte aligned id array");
+    HYT_CUDA(cudaSetDevice(g->device));
+    cudaStream_t st = g->main;
+    phase("validate");
+    EarlyStore early;
     if (g->world == 1) {
         const int dev = g->device;
         const bool weighted = w != nullptr;
-        early.th = std::thread([&early, dev, weighted, early_nbytes, early_wbytes] {
+        early.nbytes = ((E * 4 + 15) & ~15ull) + 32;
+        early.wbytes = ((E * 8 + 15) & ~15ull) + 32;
+        early.th = std::thread([&early, dev, weighted, adopt] {
             try {
                 cudaSetDevice(dev);
-                early.n = pinned_alloc(early_nbytes);
-                if (weighted) early.w = pinned_alloc(early_wbytes);
+                if (!adopt) early.n = pinned_alloc(early.nbytes);
+                if (weighted) early.w = pinned_alloc(early.wbytes);
             } catch (...) {
                 early.err = std::current_exception();
             }
@@ -391,136 +618,126 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
     try {
         vn.open(nbr, E * 4);
         if (w) vw.open(w, E * 4);
+        HYT_REQUIRE(!adopt || !vn.tmp, HYT_ENOMEM, "HYT_ADOPT_HOST: the id array could not be registered in place");
         phase("map caller arrays");
-        if (E) k_indeg<<<grid_for(E), 256, 0, st>>>((const uint32_t *)vn.dev, E, V, din, bad);
-        uint32_t bad_h = 0;
-        HYT_CUDA(cudaMemcpyAsync(&bad_h, bad, 4, cudaMemcpyDeviceToHost, st));
+        plan_phase(g, V, E, off, nullptr, nullptr, (const uint32_t *)vn.dev, flags, phase);
+        const uint32_t *adopt_ids = nullptr;
+        if (adopt) {
+            HYT_REQUIRE(g->off_h[g->store_v_lo] % 4 == 0, HYT_EINVAL,
+                        "HYT_ADOPT_HOST: this rank's first edge is not on a 16-byte chunk boundary");
+            adopt_ids = nbr + g->off_h[g->store_v_lo];
+        }
+        rows_phase(g, nullptr, (const uint32_t *)vn.dev, (const uint32_t *)vw.dev, w != nullptr, &early, adopt_ids,
+                   phase);
         HYT_CUDA(cudaStreamSynchronize(st));
-        HYT_REQUIRE(bad_h == 0, HYT_EINVAL, "neighbour id >= V");
-        if (flags & HYT_SYMMETRIC) {
-            k_sym_degrees<<<grid_for(V), 256, 0, st>>>(off_old, din, V, bad);
-            HYT_CUDA(cudaMemcpyAsync(&bad_h, bad, 4, cudaMemcpyDeviceToHost, st));
-            HYT_CUDA(cudaStreamSynchronize(st));
-            HYT_REQUIRE(bad_h == 0, HYT_EINVAL, "HYT_SYMMETRIC: some vertex's in-degree differs from its out-degree");
-        }
-        phase("in-degrees (zero-copy)");
-
-        // ---- hub sort: top h = ceil(frac*V) by D_o*D_i ----
-        const uint64_t fden = 1000000;
-        const uint64_t fnum = (uint64_t)(g->prm.hub_fraction * (double)fden + 0.5);
-        uint64_t h = (flags & HYT_NO_HUBSORT) ? 0 : (fnum * V + fden - 1) / fden;
-        if (h > V) h = V;
-        k_fill_u32<<<grid_for(V), 256, 0, st>>>(nonhub, V, 1u);
-        if (h > 0) {
-            // exact radix select of the h-th largest key T (8 passes of 8 bits), then
-            // only the h hubs are sorted: O(V) memory instead of a full-V key sort
-            unsigned long long *hist = (unsigned long long *)T(256 * 8, "load: select histogram");
-            std::vector<unsigned long long> hh(256);
-            uint64_t prefix = 0, mask = 0, kk = h;
-            for (int pass = 0; pass < 8; ++pass) {
-                const int shift = 56 - 8 * pass;
-                HYT_CUDA(cudaMemsetAsync(hist, 0, 256 * 8, st));
-                k_key_hist<<<grid_for(V, 256, num_sms() * 8), 256, 0, st>>>(off_old, din, V, prefix, mask, shift, hist);
-                HYT_CUDA(cudaMemcpyAsync(hh.data(), hist, 256 * 8, cudaMemcpyDeviceToHost, st));
-                HYT_CUDA(cudaStreamSynchronize(st));
-                unsigned long long acc = 0;
-                int d = 255;
-                for (; d > 0; --d) {
-                    if (acc + hh[d] >= kk) break;
-                    acc += hh[d];
-                }
-                kk -= acc;
-                prefix |= (uint64_t)d << shift;
-                mask |= 0xFFull << shift;
-            }
-            const uint64_t Tkey = prefix, ties = kk;      // hubs: key > T, plus `ties` of key == T by id
-            k_tie_flags<<<grid_for(V), 256, 0, st>>>(off_old, din, V, Tkey, nonhub);
-            size_t t0 = 0;
-            HYT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t0, nonhub, nonhub_scan, (int)V, st));
-            void *tsc = T(t0 + 16, "load: select scan temp");
-            HYT_CUDA(cub::DeviceScan::ExclusiveSum(tsc, t0, nonhub, nonhub_scan, (int)V, st));
-            k_hub_flags<<<grid_for(V), 256, 0, st>>>(off_old, din, V, Tkey, ties, nonhub_scan, nonhub);
-            HYT_CUDA(cub::DeviceScan::ExclusiveSum(tsc, t0, nonhub, nonhub_scan, (int)V, st));
-            uint32_t *hid = (uint32_t *)T(h * 4 + 16, "load: hub ids");
-            uint32_t *hid2 = (uint32_t *)T(h * 4 + 16, "load: hub ids sorted");
-            uint64_t *hkey = (uint64_t *)T(h * 8 + 16, "load: hub keys");
-            uint64_t *hkey2 = (uint64_t *)T(h * 8 + 16, "load: hub keys sorted");
-            k_scatter_hubs<<<grid_for(V), 256, 0, st>>>(off_old, din, V, nonhub, nonhub_scan, hid, hkey);
-            size_t tb = 0;
-            HYT_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, hkey, hkey2, hid, hid2, (int)h, 0, 64, st));
-            void *tsort = T(tb + 16, "load: hub sort temp");
-            // stable: equal keys keep ascending ids
-            HYT_CUDA(cub::DeviceRadixSort::SortPairsDescending(tsort, tb, hkey, hkey2, hid, hid2, (int)h, 0, 64, st));
-            k_fill_u32<<<grid_for(V), 256, 0, st>>>(nonhub, V, 1u);
-            k_mark_hubs<<<grid_for(h), 256, 0, st>>>(hid2, h, g->new_id_d, nonhub);
-            HYT_CUDA(cudaStreamSynchronize(st));
-            for (void *q : {(void *)tsort, (void *)hkey2, (void *)hkey, (void *)hid2, (void *)hid, tsc, (void *)hist}) {
-                A.release(q);
-                tmp.erase(std::find(tmp.begin(), tmp.end(), q));
-            }
-        }
-        uint64_t *deg2 = (uint64_t *)T((V + 1) * 8, "load: degrees");
-        size_t ts = 0;
-        HYT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, ts, nonhub, nonhub_scan, (int)V, st));
-        void *tscan = T(ts + 16, "load: scan temp");
-        HYT_CUDA(cub::DeviceScan::ExclusiveSum(tscan, ts, nonhub, nonhub_scan, (int)V, st));
-        k_finish_perm<<<grid_for(V), 256, 0, st>>>(V, h, nonhub, nonhub_scan, off_old, din, g->new_id_d,
-                                                  g->old_of_d, deg2, g->din_d);
-        size_t t2 = 0;
-        HYT_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, deg2, g->off_d, (int)(V + 1), st));
-        void *tscan2 = T(t2 + 16, "load: scan temp 2");
-        HYT_CUDA(cub::DeviceScan::ExclusiveSum(tscan2, t2, deg2, g->off_d, (int)(V + 1), st));
-        g->off_h.resize(V + 1);
-        HYT_CUDA(cudaMemcpyAsync(g->off_h.data(), g->off_d, (V + 1) * 8, cudaMemcpyDeviceToHost, st));
-        phase("hub sort + new offsets");
-
-        HYT_CUDA(cudaStreamSynchronize(st));   // off_h ready
-        // ---- pinned mapped edge store of this rank's vertex range (the
-        // whole graph at world 1), from a 16-byte chunk boundary, 16-B padded so chunk
-        // loads never overrun ----
-        rank_vertex_range(g->off_h, g->world, g->rank, &g->store_v_lo, &g->store_v_hi);
-        const uint64_t e_lo = g->off_h[g->store_v_lo], e_hi = g->off_h[g->store_v_hi];
-        g->store_c0[0] = e_lo / 4;                          // first chunk of u32 ids
-        g->store_c0[1] = e_lo / 2;                          // first chunk of u64 records
-        const uint64_t nbase = g->store_c0[0] * 4, wbase = g->store_c0[1] * 2;
-        const uint64_t nbytes = (((e_hi - nbase) * 4 + 15) & ~15ull) + 32;
-        const uint64_t wbytes = (((e_hi - wbase) * 8 + 15) & ~15ull) + 32;
-        if (early.th.joinable()) {
-            early.th.join();
-            if (early.err) std::rethrow_exception(early.err);
-            HYT_REQUIRE(nbytes == early_nbytes && (!w || wbytes == early_wbytes), HYT_ESTATE,
-                        "edge store size mismatch");
-            g->nbr_h = (uint32_t *)early.n;                 // ownership moves to the handle
-            g->ew_h = (uint64_t *)early.w;
-            early.n = early.w = nullptr;
-        } else {
-            g->nbr_h = (uint32_t *)pinned_alloc(nbytes);  // zero-filled (padding included)
-            if (w) g->ew_h = (uint64_t *)pinned_alloc(wbytes);
-        }
-        uint32_t *nbr_out = nullptr;
-        uint64_t *ew_out = nullptr;
-        HYT_CUDA(cudaHostGetDevicePointer((void **)&nbr_out, g->nbr_h, 0));
-        if (w) HYT_CUDA(cudaHostGetDevicePointer((void **)&ew_out, g->ew_h, 0));
-        phase("pin edge store");
-
-        if (e_hi > e_lo) {
-            k_relabel_tiles<<<num_sms() * 4, 512, 0, st>>>(V, e_lo, e_hi, off_old, g->off_d, g->old_of_d, g->new_id_d,
-                                                      (const uint32_t *)vn.dev, (const uint32_t *)vw.dev,
-                                                      nbr_out - nbase, ew_out ? ew_out - wbase : nullptr);
-        }
-        HYT_CUDA(cudaStreamSynchronize(st));
-        HYT_CUDA(cudaGetLastError());
-        phase("relabel edges (zero-copy)");
     } catch (...) {
-        cudaStreamSynchronize(st);
+        load_fail(g);
         vn.close(); vw.close();
-        for (auto it = tmp.rbegin(); it != tmp.rend(); ++it) A.release(*it);
         throw;
     }
+    if (adopt) {   // the caller's ids stay mapped for the handle's lifetime
+        g->adopt_key = vn.reg;
+        g->adopt_dev = vn.dev;
+        vn.reg = nullptr;
+    }
     vn.close(); vw.close();
-    for (auto it = tmp.rbegin(); it != tmp.rend(); ++it) A.release(*it);
+    load_done(g);
     phase("unmap + release");
-    g->loaded = true;
+}
+
+void load_shard_begin(hyt_graph *g, uint64_t V, const uint32_t *out_deg, const uint32_t *in_deg, uint32_t flags,
+                      uint64_t *row_lo, uint64_t *row_hi, uint64_t *edges) {
+    Phase phase{g};
+    HYT_REQUIRE(!g->loaded && !g->planned, HYT_ESTATE, "graph already loaded");
+    HYT_REQUIRE(V > 0 && V < (1ull << 32), HYT_EINVAL, "V must be in [1, 2^32)");
+    HYT_REQUIRE(out_deg && in_deg, HYT_EINVAL, "null degree array");
+    HYT_REQUIRE(!(flags & HYT_ADOPT_HOST) || (flags & HYT_NO_HUBSORT), HYT_EINVAL,
+                "HYT_ADOPT_HOST needs HYT_NO_HUBSORT");
+    HYT_CUDA(cudaSetDevice(g->device));
+    HostView vo, vi;
+    try {
+        vo.open(out_deg, V * 4);
+        vi.open(in_deg, V * 4);
+        plan_phase(g, V, 0, nullptr, out_deg, in_deg, nullptr, flags, phase);
+        HYT_CUDA(cudaStreamSynchronize(g->main));
+    } catch (...) {
+        load_fail(g);
+        vo.close(); vi.close();
+        throw;
+    }
+    vo.close(); vi.close();
+    g->ld_flags = flags;
+    g->planned = true;
+    *row_lo = g->store_v_lo;
+    *row_hi = g->store_v_hi;
+    *edges = g->off_h[g->store_v_hi] - g->off_h[g->store_v_lo];
+}
+
+void shard_rows(hyt_graph *g, uint32_t *rows, uint64_t n) {
+    HYT_REQUIRE(g->planned || g->loaded, HYT_ESTATE, "call hyt_load_shard_begin first");
+    HYT_REQUIRE(n == g->store_v_hi - g->store_v_lo, HYT_EINVAL, "row count != row_hi - row_lo");
+    HYT_CUDA(cudaSetDevice(g->device));
+    if (n) HYT_CUDA(copy_sync(rows, g->old_of_d + g->store_v_lo, n * 4, g->main));
+}
+
+void load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off, const uint32_t *nbr,
+                     const uint32_t *w) {
+    Phase phase{g};
+    HYT_REQUIRE(g->planned, HYT_ESTATE, "call hyt_load_shard_begin first");
+    HYT_REQUIRE(nrows == g->store_v_hi - g->store_v_lo, HYT_EINVAL, "row count != row_hi - row_lo");
+    HYT_REQUIRE(row_off != nullptr, HYT_EINVAL, "null row offsets");
+    HYT_CUDA(cudaSetDevice(g->device));
+    cudaStream_t st = g->main;
+    const uint64_t e_lo = g->off_h[g->store_v_lo], e_hi = g->off_h[g->store_v_hi], n_e = e_hi - e_lo;
+    HYT_REQUIRE(row_off[0] == 0 && row_off[nrows] == n_e, HYT_EINVAL,
+                "row offsets must start at 0 and end at this rank's edge count");
+    HYT_REQUIRE(n_e == 0 || nbr != nullptr, HYT_EINVAL, "null id array");
+    // every row's degree must be the one the plan used (the internal offsets)
+    for (uint64_t i = 0; i < nrows; ++i)
+        HYT_REQUIRE(row_off[i + 1] - row_off[i] == g->off_h[g->store_v_lo + i + 1] - g->off_h[g->store_v_lo + i],
+                    HYT_EINVAL, "row " + std::to_string(i) + ": degree differs from the out-degree given to begin");
+    const bool adopt = (g->ld_flags & HYT_ADOPT_HOST) != 0;
+    HYT_REQUIRE(!adopt || (e_lo % 4 == 0 && ((uintptr_t)nbr & 15) == 0), HYT_EINVAL,
+                "HYT_ADOPT_HOST needs a 16-byte aligned id array starting on a 16-byte chunk boundary of the "
+                "global edge order");
+    HostView vn, vw;
+    Temps T(g->arena);
+    try {
+        vn.open(nbr, n_e * 4);
+        if (w) vw.open(w, n_e * 4);
+        HYT_REQUIRE(!adopt || !vn.tmp, HYT_ENOMEM, "HYT_ADOPT_HOST: the id array could not be registered in place");
+        uint64_t *rs = (uint64_t *)T.get((nrows + 1) * 8 + 16, "load: row starts");
+        HYT_CUDA(copy_sync(rs, row_off, (nrows + 1) * 8, st));
+        rows_phase(g, rs, (const uint32_t *)vn.dev, (const uint32_t *)vw.dev, w != nullptr, nullptr,
+                   adopt ? nbr : nullptr, phase);
+        HYT_CUDA(cudaStreamSynchronize(st));
+    } catch (...) {
+        vn.close(); vw.close();
+        throw;
+    }
+    if (adopt) {
+        g->adopt_key = vn.reg;
+        g->adopt_dev = vn.dev;
+        vn.reg = nullptr;
+    }
+    vn.close(); vw.close();
+    load_done(g);
+}
+
+// Drop the registration of an adopted id array (hyt_free).
+void release_adopted(hyt_graph *g) {
+    if (!g->nbr_adopted) return;
+    if (g->adopt_key) {
+        std::lock_guard<std::mutex> l(g_reg_mu);
+        auto it = g_reg.find(g->adopt_key);
+        if (it != g_reg.end() && --it->second.refs == 0) {
+            cudaHostUnregister((void *)g->adopt_key);
+            g_reg.erase(it);
+        }
+    }
+    g->adopt_key = nullptr;
+    g->nbr_h = nullptr;
+    g->nbr_adopted = false;
 }
 
 }  // namespace hyt

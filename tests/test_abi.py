@@ -70,11 +70,15 @@ def test_binding_constants_match_header():
     txt = open(hyt.HEADER_PATH).read()
     defs = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define\s+(HYT_[A-Z_]+)\s+(-?\d+)u?", txt)}
     assert defs["HYT_NO_HUBSORT"] == hyt.HYT_NO_HUBSORT and defs["HYT_SYMMETRIC"] == hyt.HYT_SYMMETRIC
+    assert defs["HYT_ADOPT_HOST"] == hyt.HYT_ADOPT_HOST
     for name, val in hyt.MODES.items():
         assert defs[f"HYT_MODE_{name.upper()}"] == val, name
     for name in ("BFS", "SSSP", "CC", "PR"):
         assert defs[f"HYT_{name}"] == getattr(hyt, f"HYT_{name}")
-    # hyt_iter: 3 u64 + 6 u32 + 3 u64 + 1 double; hyt_stats ends with pull_iters, um_balloon_bytes, exch_peer
+    # hyt_iter: 3 u64 + 6 u32 + 3 u64 + 1 double; hyt_stats ends with pull_iters, um_balloon_bytes,
+    # exch_peer, host_store_bytes
     assert ctypes.sizeof(hyt.hyt_iter) == 3 * 8 + 6 * 4 + 3 * 8 + 8
-    assert [f for f, _ in hyt.hyt_stats._fields_][-3:] == ["pull_iters", "um_balloon_bytes", "exch_peer"]
+    assert [f for f, _ in hyt.hyt_stats._fields_][-4:] == ["pull_iters", "um_balloon_bytes", "exch_peer",
+                                                           "host_store_bytes"]
+    assert "uint64_t host_store_bytes;" in txt
     assert "uint64_t pull_iters, um_balloon_bytes;" in txt and "uint32_t dir;" in txt
