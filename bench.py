@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--engine", default="hybrid")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-full", action="store_true", help="skip the full-size single-core oracle SSSP")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the per-config / per-algorithm / per-engine-mode comparison runs (N=1 only)")
     ap.add_argument("--cpu-shift", type=int, default=6, help="oracle sample = the workload >> cpu_shift")
     ap.add_argument("--json-out", default="")
     ap.add_argument("--detail-out", default="", help="write per-iteration logs + stats of the last step here")
@@ -183,6 +186,42 @@ def peaks() -> dict:
 
 # --------------------------------------------------------------------------- reference arm
 
+def host_cpu() -> dict:
+    model = ""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
+def use_native_oracle() -> str:
+    """Build the oracle for this host (-O3 -march=native) and make `import oracle` load it."""
+    import tempfile
+    path = os.path.join(tempfile.gettempdir(), f"hyt_oracle_native_{os.getpid()}.so")
+    sys.path.insert(0, ROOT)
+    import oracle
+    oracle.build_native(path)
+    os.environ["ORACLE_LIB"] = path
+    oracle._lib = None
+    return path
+
+
+def cpu_oracle_full_sssp(g) -> dict:
+    """Dijkstra (the oracle as it stands) once on the FULL workload graph, one core."""
+    import oracle
+    t = time.perf_counter()
+    d = oracle.sssp(g.off, g.nbr, g.w, 0)
+    dt = time.perf_counter() - t
+    e = reached_edges(g, d)
+    return {"algo": "sssp", "graph": g.name or "full", "V": g.V, "E": g.E, "seconds": dt, "edges": e,
+            "gteps": e / dt / 1e9}
+
+
 def cpu_oracle_sample(config: str, shift: int, algos, steps: int = 1):
     """The CPU oracle (as it stands) on a bounded sample of the same workload."""
     import oracle
@@ -216,6 +255,7 @@ def run_reference(args):
         return 0
     algos = args.algos.split(",")
     shift = max(args.shift, args.cpu_shift)
+    native = use_native_oracle()
     import oracle
     g, _ = make_graph(args.config, shift, weighted=True)
     times = []
@@ -244,10 +284,74 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "u32+f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": workload_desc(args.config, args.shift, algos), "budget_gb": args.budget_gb,
                        "engine_mode": args.engine, "reference_sample": f"{args.config}>>{shift}"},
-            "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample,
+                             "host": host_cpu(), "build": f"gcc -O3 -march=native ({os.path.basename(native)})"},
             "e2e": {"value": val, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+# --------------------------------------------------------------------------- per-config comparison
+
+# (config, device budget GB, algorithms): BASELINE.json configs[1..3] at one GPU
+EXTRAS = [("tw", 16, ["sssp", "pr"]), ("fr", 4, ["bfs", "cc"]), ("uk", 8, ["sssp", "pr"])]
+
+
+def run_extras(hyt, local: int, tw_graph=None) -> dict:
+    """One timed run per (config, algorithm, engine mode): the hybrid against the pure
+    explicit (filter, compaction) and implicit (zero-copy) modes of the same build, with
+    the host-link transfer volume normalised to the edge volume (Table V / Table VI
+    analogs).  Results must agree across modes."""
+    import torch
+    out = {}
+    for name, bgb, algos in EXTRAS:
+        t = time.time()
+        g = tw_graph if (name == "tw" and tw_graph is not None) else \
+            make_graph(name, 0, weighted=("sssp" in algos))[0]
+        gen_s = time.time() - t
+        G = hyt.Graph(device=local, budget=int(bgb * (1 << 30)))
+        t = time.time()
+        G.load(g.off, g.nbr, g.w if "sssp" in algos else None, symmetric=bool(g.symmetric))
+        load_s = time.time() - t
+        cur = torch.cuda.current_stream()
+        res = {}
+        for a in algos:
+            modes = ["hybrid", "filter", "zerocopy"] + ([] if a == "pr" else ["compaction"])
+            row, ref = {}, None
+            for m in modes:
+                G.set("engine_mode", m)
+                torch.cuda.synchronize()
+                s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s_ev.record(cur)
+                G.run(a, 0)
+                e_ev.record(cur)
+                torch.cuda.synchronize()
+                sec = s_ev.elapsed_time(e_ev) / 1e3
+                st = G.stats()
+                vals = G.values()
+                edges = reached_edges(g, vals) if a in ("sssp", "bfs") else g.E
+                d1 = 8 if a == "sssp" else 4
+                xfer = st["bytes_filter"] + st["bytes_compaction"] + st["bytes_zerocopy"]
+                if ref is None:
+                    ref, agree = vals, True
+                elif a == "pr":
+                    agree = bool(np.max(np.abs(vals - ref) / np.maximum(ref, 1e-30)) < 2e-4)
+                else:
+                    agree = bool(np.array_equal(vals, ref))
+                row[m] = {"s": sec, "gteps": edges / sec / 1e9, "iterations": int(st["iterations"]),
+                          "xfer_over_edge_volume": xfer / (g.E * d1), "agrees_with_hybrid": agree,
+                          "parts_fcz": [int(st["parts_filter"]), int(st["parts_compaction"]),
+                                        int(st["parts_zerocopy"])]}
+            others = [row[m]["s"] for m in modes if m != "hybrid"]
+            row["hybrid_fastest"] = bool(row["hybrid"]["s"] <= min(others))
+            row["speedup_vs_best_pure"] = min(others) / row["hybrid"]["s"]
+            res[a] = row
+        G.close()
+        out[name] = {"workload": workload_desc(name, 0, algos), "budget_gb": bgb, "gen_s": gen_s,
+                     "load_s": load_s, "algos": res}
+        if g is not tw_graph:
+            del g
+    return out
 
 
 # --------------------------------------------------------------------------- our arm
@@ -461,10 +565,18 @@ def main():
                  "unit": "GB/s", "frac": link_bytes / total_s / 1e9 / h2d_peak,
                  "note": "algorithmic host-link bytes (filter spans + compacted chunks + zero-copy lines) / step time"}
 
+    extras = None
+    if world == 1 and not args.no_extras and args.shift == 0 and args.config == "tw":
+        extras = run_extras(hyt, local, tw_graph=g)
+
     cpu = None
     if not args.no_cpu_baseline:
         try:
+            native = use_native_oracle()
             cpu = cpu_oracle_sample(args.config, max(args.shift, args.cpu_shift), algos)
+            cpu.update({"host": host_cpu(), "build": f"gcc -O3 -march=native ({os.path.basename(native)})"})
+            if not args.no_cpu_full:
+                cpu["full_size"] = cpu_oracle_full_sssp(g)
         except Exception as ex:
             cpu = {"error": repr(ex)}
 
@@ -494,6 +606,7 @@ def main():
         "host_link": host_link,
         "engine_ms": {tags[i]: float(eng_ms[i]) for i in range(8)},
         "cpu_baseline": cpu,
+        "extras": extras,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -26,10 +26,25 @@ INF32 = 0xFFFFFFFF
 NONE, F, C, Z = 0, 1, 2, 3
 
 
+_FLAGS = ["-O3", "-march=x86-64-v3", "-ffp-contract=off", "-fPIC", "-shared", "-pthread"]
+
+
 def build(force: bool = False) -> str:
+    """liboracle.so (the Makefile's flags).  ORACLE_LIB=<path> loads another build of
+    the same oracle.c instead (bench.py's cpu_baseline compiles one with
+    -march=native on the box it runs on)."""
+    if os.environ.get("ORACLE_LIB"):
+        return os.environ["ORACLE_LIB"]
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fPIC", "-shared", "-o", _SO, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *_FLAGS, "-o", _SO, _SRC, "-lm"])
     return _SO
+
+
+def build_native(path: str) -> str:
+    """The same oracle.c built for the host it runs on (-O3 -march=native), for timing."""
+    subprocess.check_call(["gcc", "-O3", "-march=native", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
+                           "-o", path, _SRC, "-lm"])
+    return path
 
 
 class _CostCfg(ctypes.Structure):
@@ -62,8 +77,7 @@ _lib = None
 def _L():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_SO)
+        L = ctypes.CDLL(build())
         u64, vp, i32 = ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int
         L.oracle_bfs.argtypes = [u64, vp, vp, u64, vp]
         L.oracle_sssp.argtypes = [u64, vp, vp, vp, u64, vp]

@@ -132,7 +132,12 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "relax_ctas_per_sm") { integral(); in(1, 32); p.relax_ctas_per_sm = (int)v; }
         else if (k == "exchange") { integral(); in(0, 3); p.exchange = (int)v; }
         else if (k == "relax_hot") { integral(); in(0, 2); p.relax_hot = (int)v; }
-        else if (k == "relax_hot_v") { integral(); in(32, 12288); p.relax_hot_v = (uint64_t)v; }
+        else if (k == "relax_hot_v") { integral(); in(32, 20480); p.relax_hot_v = (uint64_t)v; }
+        else if (k == "relax_threads") {
+            integral();
+            HYT_REQUIRE(v == 512 || v == 1024, HYT_EINVAL, "relax_threads must be 512 or 1024");
+            p.relax_threads = (int)v;
+        }
         else if (k == "edge_cache") { integral(); in(0, 1); p.edge_cache = (int)v; }
         else if (k == "edge_cache_bytes") { integral(); in(0, 1e13); p.edge_cache_bytes = (uint64_t)v; }
         else if (k == "cpu_cost") { integral(); in(0, 1); p.cpu_cost = (int)v; }

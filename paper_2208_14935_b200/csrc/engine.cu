@@ -667,6 +667,7 @@ static DevState make_state(hyt_graph *g, RunCtx *c) {
     s.damping = (float)g->prm.damping;
     s.epsilon = (float)g->prm.epsilon;
     s.hot_v = (uint32_t)g->prm.relax_hot_v;
+    s.relax_nt = g->prm.relax_threads;
     return s;
 }
 

@@ -72,6 +72,7 @@ struct Params {
                                // 3 fused peer push (relax writes remote destinations into their owner's memory)
     int relax_hot = 1;         // hub block in smem (PR Δ accumulation / min-algorithm value copy): 0 off, 1 auto, 2 always
     uint64_t relax_hot_v = 8192;    // PR hub-block vertices in shared memory (8 B each: 64 KB; min-algorithms cap at kHotV)
+    int relax_threads = 512;        // relax CTA size (512: 2 CTAs/SM, 1024: 1 CTA/SM sharing a larger hub block)
     int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
     uint64_t edge_cache_bytes = 0;   // cap on the cache (0 = whatever the budget leaves)
     int cpu_cost = 0;          // 1: include Eq. 2's CPU term with Thpt_cpt calibrated on this box

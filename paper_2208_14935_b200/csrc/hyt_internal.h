@@ -16,8 +16,6 @@ namespace hyt {
 // line (the EMOGI "merged and aligned" access).
 // ---------------------------------------------------------------------------
 constexpr int kChunkBytes = 16;
-constexpr int kRelaxThreads = 512;      // threads per relax CTA (16 independent warps sharing one hub block)
-constexpr int kRelaxMinBlocks = 2;      // 2 x 512 threads per SM: 64 registers per thread
 constexpr int kChunksPerThread = 4;     // 16-byte loads in flight per lane
 constexpr int kTile = 32 * kChunksPerThread;   // chunks per WARP tile (2 KiB of edges)
 #ifndef HYT_HOTV
@@ -128,6 +126,7 @@ struct DevState {
     int algo;
     float damping, epsilon;
     uint32_t hot_v;             // hub-block size in shared memory (relax_hot_v)
+    int relax_nt;               // relax CTA size: 512 or 1024 threads (relax_threads)
 };
 
 // Fused multi-rank push (exchange = 3): a destination outside the own range

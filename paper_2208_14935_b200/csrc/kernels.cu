@@ -69,7 +69,6 @@ struct RelaxArgs {
     PeerPush pp;               // fused multi-rank push (PEER instantiations only)
 };
 
-constexpr int kWarps = kRelaxThreads / 32;
 
 // L2 eviction-priority hints: the edge stream is read once per task (evict first),
 // the vertex values / deltas are re-read by every task (evict last), so the
@@ -143,16 +142,18 @@ __device__ __forceinline__ void hub_add_fx(uint32_t *lo, uint32_t *hi, uint32_t 
     if (old + xlo < old) atomicAdd(&hi[d], 1u);
 }
 
-template <int ALGO, bool COMPACT, bool PEER>
-__global__ void __launch_bounds__(kRelaxThreads, kRelaxMinBlocks)
+template <int ALGO, bool COMPACT, bool PEER, int NT>
+__global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
 k_relax(RelaxArgs A) {
     constexpr uint32_t D1 = (ALGO == ALGO_SSSP) ? 8u : 4u;
     constexpr int EPC = 16 / D1;                  // edge records per chunk
     constexpr bool PR = (ALGO == ALGO_PR);
-    __shared__ WarpStage s_st[kWarps];
-    // hub block (dynamic): PR = n_hot lo words then n_hot hi words (fixed point);
-    // min-algorithms = n_hot hub values
-    extern __shared__ uint32_t s_hotw[];
+    constexpr int kWarps = NT / 32;
+    // dynamic shared memory: the warps' staging, then the hub block (PR = n_hot lo
+    // words then n_hot hi words, fixed point; min-algorithms = n_hot hub values)
+    extern __shared__ __align__(16) uint8_t s_dyn[];
+    WarpStage *s_st = reinterpret_cast<WarpStage *>(s_dyn);
+    uint32_t *s_hotw = reinterpret_cast<uint32_t *>(s_dyn + kWarps * sizeof(WarpStage));
     const DevState &S = A.s;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpStage &W = s_st[w];
@@ -337,7 +338,7 @@ k_relax(RelaxArgs A) {
 // Launch with a dynamic hub block of `smem` bytes: raise the kernel's dynamic shared
 // memory limit once, and cap the persistent grid at what stays resident (a second
 // wave of a grid-stride kernel would double the tail).
-static void relax_go(void (*k)(RelaxArgs), const RelaxArgs &A, uint64_t grid, size_t smem, cudaStream_t st) {
+static void relax_go(void (*k)(RelaxArgs), int nt, const RelaxArgs &A, uint64_t grid, size_t smem, cudaStream_t st) {
     // cached per (device, kernel, smem): the attribute and the occupancy belong to a
     // device context, and one thread may drive handles on several GPUs
     struct Occ { int dev; void (*k)(RelaxArgs); size_t smem; int per_sm; };
@@ -349,18 +350,23 @@ static void relax_go(void (*k)(RelaxArgs), const RelaxArgs &A, uint64_t grid, si
     for (int i = 0; i < ncache; ++i)
         if (cache[i].dev == dev && cache[i].k == k && cache[i].smem == smem) { per_sm = cache[i].per_sm; break; }
     if (per_sm < 0) {
-        // raise the dynamic limit only past the 48 KB default (a raised limit can shift
-        // the L1 / shared-memory carveout of every later launch)
+        // past the 48 KB default, allow the kernel the device's opt-in maximum (one
+        // setting serves every hub-block size of this kernel on this device)
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, k);
-        if (fa.sharedSizeBytes + smem > 48 * 1024)
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kRelaxThreads, smem) != cudaSuccess || per_sm < 1)
+        if (fa.sharedSizeBytes + smem > 48 * 1024) {
+            int optin = 0;
+            if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+                optin < 1)
+                optin = 227 * 1024;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes);
+        }
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, nt, smem) != cudaSuccess || per_sm < 1)
             per_sm = 1;
         if (ncache < 128) cache[ncache++] = Occ{dev, k, smem, per_sm};
     }
     if (grid > (uint64_t)num_sms() * per_sm) grid = (uint64_t)num_sms() * per_sm;
-    k<<<(unsigned)grid, kRelaxThreads, smem, st>>>(A);
+    k<<<(unsigned)grid, nt, smem, st>>>(A);
 }
 
 void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uint64_t seg_first,
@@ -373,12 +379,15 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     A.c_lo = c_lo; A.c_hi = c_hi; A.seg_chunks = seg_chunks; A.seg_first = seg_first; A.seg_end = seg_end;
     A.dev_tot = dev_tot; A.base = src.base; A.shift = src.shift;
     if (peer) A.pp = *peer;
+    const int nt = s.relax_nt >= 1024 ? 1024 : 512;      // threads per CTA (relax_threads)
+    const uint64_t nwarps = (uint64_t)nt / 32;
+    if (nt == 1024) max_ctas = (max_ctas + 1) / 2;           // same threads per SM
     uint64_t grid;
     if (dev_tot) grid = (uint64_t)max_ctas;
     else {
         if (c_hi <= c_lo) return;
         const uint64_t tiles = (c_hi - 1) / kTile - c_lo / kTile + 1;
-        grid = (tiles + kWarps - 1) / kWarps;
+        grid = (tiles + nwarps - 1) / nwarps;
         if (grid > (uint64_t)max_ctas) grid = (uint64_t)max_ctas;
     }
     if (grid == 0) grid = 1;
@@ -392,11 +401,15 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     const uint64_t hv = s.V < hv_cap ? s.V : hv_cap;
     A.n_hot = 0;
     if (hot && s.algo == ALGO_PR) A.n_hot = (uint32_t)hv;
-    else if (hot == 2 || (hot == 1 && !dev_tot && (c_hi - c_lo) >= grid * kWarps * 4 * kTile)) A.n_hot = (uint32_t)hv;
-    const size_t smem = (size_t)A.n_hot * (s.algo == ALGO_PR ? 8 : 4);   // PR: fixed-point (lo, hi) pairs
+    else if (hot == 2 || (hot == 1 && !dev_tot && (c_hi - c_lo) >= grid * nwarps * 4 * kTile)) A.n_hot = (uint32_t)hv;
+    // staging of every warp + the hub block (PR: fixed-point (lo, hi) pairs)
+    const size_t smem = nwarps * sizeof(WarpStage) + (size_t)A.n_hot * (s.algo == ALGO_PR ? 8 : 4);
+#define HYT_RELAX_N(ALG, CO, PE)                                                                 \
+    if (nt == 1024) relax_go(k_relax<ALG, CO, PE, 1024>, nt, A, grid, smem, st);              \
+    else relax_go(k_relax<ALG, CO, PE, 512>, nt, A, grid, smem, st);
 #define HYT_RELAX_B(ALG, PE)                                                                     \
-    if (src.compact) relax_go(k_relax<ALG, true, PE>, A, grid, smem, st);                     \
-    else relax_go(k_relax<ALG, false, PE>, A, grid, smem, st);
+    if (src.compact) { HYT_RELAX_N(ALG, true, PE) }                                              \
+    else { HYT_RELAX_N(ALG, false, PE) }
 #define HYT_RELAX(ALG)                                                                           \
     if (peer && peer->n) { HYT_RELAX_B(ALG, true) }                                              \
     else { HYT_RELAX_B(ALG, false) }
@@ -406,6 +419,7 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
         case ALGO_CC: HYT_RELAX(ALGO_CC); break;
         default: HYT_RELAX(ALGO_PR); break;
     }
+#undef HYT_RELAX_N
 #undef HYT_RELAX_B
 #undef HYT_RELAX
 }

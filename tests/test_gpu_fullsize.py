@@ -9,9 +9,12 @@ fixed-point residual; plus exact oracle values on a sample of vertices whose
 answer the oracle can compute alone (vertices with in-degree 0: rank exactly 1-d;
 the source's distance 0 / level 0; unreachable vertices INF).
 
-FR- and UK-shaped graphs (configs[2], configs[3]) run at 1/8 and 1/16 scale with
-element-wise parity against the oracle (their full sizes need 60-75 GB of host
-memory per process; HYT_FULLSIZE=1 runs them at full size with certificates)."""
+Element-wise parity against the oracle at reduced scale, in the bench's launch
+configuration under oversubscribing budgets: TW at 1/8 (PR per vertex), FR at 1/4
+(CC + BFS bit-exact, CC also through the complete certificate), UK at 1/16 (PR per
+vertex + SSSP bit-exact).  PR is compared with the pull-form Jacobi oracle (O4a',
+threaded), which finishes these sizes in about a minute.  HYT_FULLSIZE=1 runs them
+at full size."""
 import functools
 import os
 
@@ -76,33 +79,48 @@ def test_tw_pr_residual_and_samples(tw_runs):
 
 
 def _scaled_parity(hyt, name, shift, algos, budget):
+    """Element-wise parity against the oracle at 1/2**shift of a BASELINE config, in
+    bench.py's launch configuration (hybrid, 32 MiB partitions) under a budget that
+    oversubscribes the device: BFS/SSSP/CC bit-exact, PR <= 1e-4 relative per vertex
+    against the pull-form Jacobi fixed point (oracle O4a', tol 1e-10 absolute)."""
     g = hytgen.make(name, shift=shift, weighted=("sssp" in algos))
     G = hyt.Graph(device=0, budget=budget)
     try:
-        G.load(g.off, g.nbr, g.w)
+        G.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
         for a in algos:
             G.run(a, 0)
             got = G.values()
+            st = G.stats()
+            assert st["device_bytes_peak"] <= budget
+            assert st["parts_filter"] + st["parts_zerocopy"] + st["parts_compaction"] > 0   # edges from host
             if a == "cc":
-                assert np.array_equal(got, oracle.cc(g.off, g.nbr))
+                want = oracle.cc(g.off, g.nbr)
+                assert np.array_equal(got, want)
+                assert oracle.check_cc(g.off, g.nbr, got) == 0
             elif a == "bfs":
                 assert np.array_equal(got, oracle.bfs(g.off, g.nbr, 0))
             elif a == "sssp":
                 assert np.array_equal(got, oracle.sssp(g.off, g.nbr, g.w, 0))
             else:
-                want, _ = oracle.pr_jacobi(g.off, g.nbr, tol=1e-11)
-                assert np.max(np.abs(got - want) / want) < 1e-4
-            st = G.stats()
-            assert st["device_bytes_peak"] <= budget
+                want, _ = oracle.pr_jacobi_pull(g.off, g.nbr, tol=1e-10)
+                rel = np.abs(got.astype(np.float64) - want) / want
+                assert rel.max() < 1e-4, (rel.max(), int(rel.argmax()))
     finally:
         G.close()
 
 
-def test_fr_shape_cc_bfs(hyt):
-    """FR-shaped (undirected, lower skew) at 1/8 scale under a 1 GB cap (1.8 GB of ids: oversubscribed)."""
-    _scaled_parity(hyt, "fr", 0 if FULL else 3, ["cc", "bfs"], (4 << 30) if FULL else (1 << 30))
+def test_tw_shift3_pr_elementwise(hyt):
+    """TW recipe at 1/8 (5.2M V, 184M edges) under 2 GB (16 GB / 8): PR per vertex."""
+    _scaled_parity(hyt, "tw", 0 if FULL else 3, ["pr"], (16 << 30) if FULL else (2 << 30))
 
 
-def test_uk_shape_pr_sssp(hyt):
-    """UK-shaped (high skew) at 1/64 scale under a 384 MB cap (467 MB of SSSP records: oversubscribed)."""
-    _scaled_parity(hyt, "uk", 0 if FULL else 6, ["pr", "sssp"], (8 << 30) if FULL else (384 << 20))
+def test_fr_shift2_cc_bfs(hyt):
+    """FR recipe at 1/4 (16.4M V, 903M stored edges) under 1 GB (3.6 GB of ids:
+    oversubscribed): CC and BFS bit-exact, CC also through the complete certificate."""
+    _scaled_parity(hyt, "fr", 0 if FULL else 2, ["cc", "bfs"], (4 << 30) if FULL else (1 << 30))
+
+
+def test_uk_shift4_pr_sssp(hyt):
+    """UK recipe at 1/16 (6.6M V, 234M edges) under 512 MB (1.9 GB of SSSP records):
+    PR per vertex and SSSP bit-exact."""
+    _scaled_parity(hyt, "uk", 0 if FULL else 4, ["pr", "sssp"], (8 << 30) if FULL else (512 << 20))

@@ -98,9 +98,12 @@ int main() {
     cudaEventCreate(&b);
     printf("{\"V\": %llu, \"E\": %llu, \"sms\": %d", (unsigned long long)V, (unsigned long long)E, sms);
     const char *names[4] = {"stream", "red_add", "ld", "ld_min"};
-    for (int skew = 0; skew < 2; ++skew) {
-        k_gen<<<sms * 8, 256>>>(idx, E, V, skew);
-        printf(", \"%s\": {", skew ? "rmat" : "uniform");
+    // third case: uniform over 16M slots (64 MB, L2-resident): the L2 rate of the
+    // pattern without DRAM misses
+    const uint64_t V_l2 = 16u << 20;
+    for (int skew = 0; skew < 3; ++skew) {
+        k_gen<<<sms * 8, 256>>>(idx, E, skew == 2 ? V_l2 : V, skew == 1);
+        printf(", \"%s\": {", skew == 1 ? "rmat" : skew == 2 ? "uniform_l2_resident" : "uniform");
         for (int op = 0; op < 4; ++op) {
             float best = 1e30f;
             for (int rep = 0; rep < 3; ++rep) {
