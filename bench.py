@@ -130,8 +130,66 @@ def make_graph(config: str, shift: int, weighted: bool):
 
 
 def reached_edges(g, dist) -> int:
-    deg = np.diff(g.off.astype(np.int64))
+    deg = g.deg if isinstance(g, Workload) else np.diff(g.off.astype(np.int64))
     return int(deg[dist != 0xFFFFFFFF].sum())
+
+
+class Workload:
+    """The graph as this rank holds it.  N = 1: the whole CSR (hyt_load_csr).  N > 1:
+    the shard load (include/hyt.h) -- each rank counts the degrees of its slice of
+    edge indices, the ranks all-reduce the O(V) degree vectors, the library names the
+    rows the rank serves and the rank regenerates only those (hytgen.rmat_rows), so
+    no process holds the whole graph (BASELINE configs[4])."""
+
+    def __init__(self, config, shift, weighted, world=1, rank=0, local=0):
+        import hytgen
+        t = time.time()
+        self.c = hytgen.recipe(config, shift)
+        self.weighted, self.world, self.rank = weighted, world, rank
+        self.V, self.symmetric = self.c["V"], bool(self.c["symmetric"])
+        self.shard = world > 1
+        self.g = None
+        self.rows = self.loff = self.lnbr = self.lw = None
+        if not self.shard:
+            self.g = hytgen.make(config, shift=shift, weighted=weighted)
+            self.deg = np.diff(self.g.off.astype(np.int64))
+        else:
+            import torch
+            import torch.distributed as dist
+            E = self.c["E"]
+            od, idg = hytgen.rmat_degrees(self.c, E * rank // world, E * (rank + 1) // world)
+            t2 = torch.from_numpy(np.stack([od, idg]).view(np.int32)).to(f"cuda:{local}")
+            dist.all_reduce(t2)                      # degrees < 2^31: int32 sums are exact
+            both = t2.cpu().numpy().view(np.uint32)
+            self.od, self.idg = np.ascontiguousarray(both[0]), np.ascontiguousarray(both[1])
+            self.deg = self.od.astype(np.int64)
+        self.E = int(self.deg.sum())
+        self.gen_s = time.time() - t
+
+    def load(self, G):
+        if not self.shard:
+            g = self.g
+            G.load(g.off, g.nbr, g.w if self.weighted else None, symmetric=self.symmetric)
+            return
+        import hytgen
+        info = G.load_shard_begin(self.od, self.idg, symmetric=self.symmetric)
+        if self.rows is None:                       # first load: generate this rank's rows
+            t = time.time()
+            self.rows = G.shard_rows(info["row_hi"] - info["row_lo"])
+            self.loff, self.lnbr, self.lw = hytgen.rmat_rows(self.c, self.rows, self.od, weighted=self.weighted)
+            self.gen_s += time.time() - t
+        G.load_shard_rows(self.loff, self.lnbr, self.lw)
+
+    def host_arrays(self):
+        if not self.shard:
+            return [self.g.off, self.g.nbr, self.g.w if self.weighted else None]
+        return [self.loff, self.lnbr, self.lw, self.od, self.idg]
+
+    def degree_stats(self) -> dict:
+        d = self.deg
+        return {"V": self.V, "E": self.E, "pct_deg_lt8": 100.0 * float((d < 8).mean()),
+                "pct_deg_lt32": 100.0 * float((d < 32).mean()), "pct_deg0": 100.0 * float((d == 0).mean()),
+                "max_deg": int(d.max()), "load": "shard (per-rank rows)" if self.shard else "full CSR"}
 
 
 def measured_h2d_gbs(device: int) -> float:
@@ -318,7 +376,9 @@ def run_extras(hyt, local: int, tw_graph=None) -> dict:
         for a in algos:
             modes = ["hybrid", "filter", "zerocopy"] + ([] if a == "pr" else ["compaction"])
             row, ref = {}, None
-            for m in modes:
+            G.set("engine_mode", "hybrid")
+            G.run(a, 0)        # untimed: run context + this graph's host-gather calibration
+            for m in modes:     # the transfer modes share the run context (no rebuild)
                 G.set("engine_mode", m)
                 torch.cuda.synchronize()
                 s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -376,7 +436,7 @@ def main():
     # ---- inputs (host), generation not timed ----
     if world > 1:
         os.environ.setdefault("HYTGEN_THREADS", str(max(1, (os.cpu_count() or 8) // world)))
-    g, gen_s = make_graph(args.config, args.shift, weighted=True)
+    g = Workload(args.config, args.shift, True, world, rank, local)
     dstats = g.degree_stats()
 
     def new_handle():
@@ -393,8 +453,9 @@ def main():
 
     G = new_handle()
     t = time.time()
-    G.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
+    g.load(G)
     load_s = time.time() - t
+    gen_s = g.gen_s
 
     def barrier():
         if world > 1:
@@ -482,14 +543,14 @@ def main():
         G.close()
         # the contract's inputs live in pinned host memory: page-lock the caller's CSR
         # arrays once, outside the timed region (hyt_load_csr then reads them in place)
-        pinned = pin_host([g.off, g.nbr, g.w])
+        pinned = pin_host(g.host_arrays())
         e2e_ms = []
         for _ in range(args.e2e_steps):
             barrier()
             s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s_ev.record(cur)
             H = new_handle()
-            H.load(g.off, g.nbr, g.w, symmetric=bool(g.symmetric))
+            g.load(H)
             step(H, out_bufs)
             e_ev.record(cur)
             barrier()
@@ -500,12 +561,15 @@ def main():
             tt = torch.tensor([em], device=f"cuda:{local}")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             em = float(tt.item())
-        h2d = g.off.nbytes + g.nbr.nbytes + g.w.nbytes
+        h2d = sum(a.nbytes for a in g.host_arrays() if a is not None)
         unpin_host(pinned)
         e2e = {"value": edges_step / (em / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": em,
-               "inputs_pinned": len(pinned) == 3,
+               "inputs_pinned": len(pinned) == len([a for a in g.host_arrays() if a is not None]),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * g.V * len(algos)),
-               "includes": "hyt_load_csr from pinned host arrays (GPU hub sort + relabel into the library's pinned edge store) + runs + hyt_get_values"}
+               "includes": ("hyt_load_shard_begin + hyt_load_shard_rows from this rank's pinned rows" if g.shard else
+                            "hyt_load_csr from pinned host arrays") +
+                           " (GPU hub sort + relabel into the library's pinned edge store) + runs + hyt_get_values",
+               "note": "the caller's arrays are page-locked once outside the timed region (inputs in pinned host memory)"}
     else:
         G.close()
 
@@ -567,7 +631,7 @@ def main():
 
     extras = None
     if world == 1 and not args.no_extras and args.shift == 0 and args.config == "tw":
-        extras = run_extras(hyt, local, tw_graph=g)
+        extras = run_extras(hyt, local, tw_graph=g.g)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -576,7 +640,7 @@ def main():
             cpu = cpu_oracle_sample(args.config, max(args.shift, args.cpu_shift), algos)
             cpu.update({"host": host_cpu(), "build": f"gcc -O3 -march=native ({os.path.basename(native)})"})
             if not args.no_cpu_full:
-                cpu["full_size"] = cpu_oracle_full_sssp(g)
+                cpu["full_size"] = cpu_oracle_full_sssp(g.g)
         except Exception as ex:
             cpu = {"error": repr(ex)}
 

@@ -234,13 +234,14 @@ int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off_ho
  *   halved down to 256 MiB if the host cannot pin it; if nothing can be pinned
  *   the rates measured on the B200 pool are used and the run proceeds);
  *   0 is the paper's rule with its PCIe-3 constants.
- *   Kernel tuning (no effect on results): relax_ctas_per_sm [4],
- *   zc_ctas_per_sm [2], relax_minb [4] (__launch_bounds__ min CTAs/SM, 4..6),
- *   relax_hot [1] (hub block ids < relax_hot_v in shared memory: PR delta
- *   accumulation, min-algorithm value copy; 0 off, 1 auto, 2 always),
- *   relax_hot_v [16384] (PR hub-block vertices, 32..32768, 4 B of dynamic
- *   shared memory each; min-algorithms use at most 4096; the persistent grid
- *   is capped at what stays resident).
+ *   Kernel tuning (no effect on results): relax_ctas_per_sm [2] (in units of
+ *   512 threads), zc_ctas_per_sm [1], relax_threads [0] (relax CTA size: 0 auto
+ *   = 1024 for PR, 512 otherwise; 512; 1024), relax_hot [1] (hub block ids <
+ *   relax_hot_v in shared memory: PR delta accumulation in fixed point,
+ *   min-algorithm value copy; 0 off, 1 auto, 2 always), relax_hot_v [16384]
+ *   (PR hub-block vertices, 32..20480, 8 B of dynamic shared memory each;
+ *   min-algorithms use at most 4096; the persistent grid is capped at what
+ *   stays resident).
  *   exchange [1] (world > 1): 0 always the dense V-entry
  *   all-reduce; 1 per iteration, all-gather the (id, value) pairs each rank
  *   changed when their bytes (world x max pairs x 8) are below the dense
@@ -306,6 +307,15 @@ int hyt_debug_plan(hyt_graph *g, int algo, const uint8_t *active_host, uint64_t 
  * units_host receives pairs (first, one-past-last); returns the unit count
  * (>= 0) or HYT_EINVAL.  Needs no GPU. */
 int64_t hyt_combine(const uint8_t *p_host, uint64_t n, uint64_t k, uint64_t *units_host);
+
+/* Contribution-driven ordering of the filter units, the host
+ * routine the scheduler uses, exposed for CPU tests: units_host holds nu pairs
+ * (first, one-past-last partition) as hyt_combine returns them, part_score_host
+ * one score per partition (hub-driven: sum of D_o*D_i over its active vertices;
+ * delta-driven: sum of their deltas).  order_host[0..nu) receives the unit
+ * indices by descending score (sum over the unit's partitions), ties by unit
+ * index.  Returns HYT_OK or HYT_EINVAL.  Needs no GPU. */
+int hyt_order_units(int64_t nu, const uint64_t *units_host, const double *part_score_host, uint32_t *order_host);
 
 /* Engine selection for one partition (section 5.1), the exact
  * integer rule the GPU selection kernel evaluates, exposed for CPU tests.

@@ -79,6 +79,7 @@ _SIGS = {
     "hyt_get_perm": ([_vp, _vp, _u64], _i32),
     "hyt_debug_plan": ([_vp, _i32, _vp, ctypes.POINTER(_u64), _vp, _vp, _vp, _vp, _vp, _vp], _i32),
     "hyt_combine": ([_vp, _u64, _u64, _vp], ctypes.c_int64),
+    "hyt_order_units": ([ctypes.c_int64, _vp, _vp, _vp], _i32),
     "hyt_select_engine": ([_vp, _u64, _u64, _u64, _u64, _u64], _i32),
     "hyt_nccl_unique_id": ([_vp], _i32),
     "hyt_rank_range": ([_vp, _u64, _u64, _u64, _i32, _i32] + [ctypes.POINTER(_u64)] * 4, ctypes.c_int64),
@@ -274,6 +275,16 @@ def combine(p, k: int = 4) -> list:
     units = np.empty(2 * len(p) + 2, dtype=np.uint64)
     n = check(hyt_combine(_ptr(p) if len(p) else None, len(p), k, _ptr(units)), "hyt_combine")
     return [(int(units[2 * j]), int(units[2 * j + 1])) for j in range(n)]
+
+
+def order_units(units, part_score) -> list:
+    """The scheduler's unit order (host routine, no GPU)."""
+    nu = len(units)
+    u = np.array([x for pr in units for x in pr] or [0], dtype=np.uint64)
+    s = np.ascontiguousarray(part_score, dtype=np.float64)
+    order = np.empty(max(1, nu), dtype=np.uint32)
+    check(hyt_order_units(nu, _ptr(u), _ptr(s), _ptr(order)), "hyt_order_units")
+    return order[:nu].tolist()
 
 
 def select_engine(t: int, e: int, a: int, z: int, d1: int) -> int:

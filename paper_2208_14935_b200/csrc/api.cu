@@ -106,6 +106,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         HYT_REQUIRE(g && key, HYT_EINVAL, "null argument");
         Params &p = g->prm;
         const std::string k(key);
+        const int old_mode = p.engine_mode;
         auto in = [&](double lo, double hi) {
             HYT_REQUIRE(v >= lo && v <= hi, HYT_EINVAL, k + " out of range");
         };
@@ -135,7 +136,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "relax_hot_v") { integral(); in(32, 20480); p.relax_hot_v = (uint64_t)v; }
         else if (k == "relax_threads") {
             integral();
-            HYT_REQUIRE(v == 512 || v == 1024, HYT_EINVAL, "relax_threads must be 512 or 1024");
+            HYT_REQUIRE(v == 0 || v == 512 || v == 1024, HYT_EINVAL, "relax_threads must be 0 (auto), 512 or 1024");
             p.relax_threads = (int)v;
         }
         else if (k == "edge_cache") { integral(); in(0, 1); p.edge_cache = (int)v; }
@@ -156,7 +157,12 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "um_balloon") { integral(); in(0, 1); p.um_balloon = (int)v; }
         else if (k == "um_cold") { integral(); in(0, 1); p.um_cold = (int)v; }
         else throw Err{HYT_EINVAL, "unknown parameter '" + k + "'"};
-        if (g->loaded) release_run_ctx(g);   // buffers depend on the parameters
+        // buffers depend on the parameters -- except a switch among the four transfer
+        // modes (hybrid / filter / compaction / zero-copy), which share one buffer
+        // layout as long as no partial edge cache is built (hybrid only)
+        auto transfer = [](int m) { return m >= MODE_HYBRID && m <= MODE_ZEROCOPY; };
+        const bool keep = k == "engine_mode" && transfer(old_mode) && transfer(p.engine_mode) && !p.edge_cache;
+        if (g->loaded && !keep) release_run_ctx(g);
     })
 }
 
@@ -206,6 +212,13 @@ int hyt_debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_
         HYT_REQUIRE(g && num_parts, HYT_EINVAL, "null argument");
         HYT_REQUIRE(active || (!bounds && !t && !p), HYT_EINVAL, "null frontier");
         debug_plan(g, algo, active, num_parts, bounds, t, e, a, z, p);
+    })
+}
+
+int hyt_order_units(int64_t nu, const uint64_t *units, const double *part_score, uint32_t *order) {
+    HYT_GUARD({
+        HYT_REQUIRE(nu >= 0 && (nu == 0 || (units && part_score && order)), HYT_EINVAL, "bad arguments");
+        order_units(nu, units, part_score, order);
     })
 }
 

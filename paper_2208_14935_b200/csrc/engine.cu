@@ -159,6 +159,19 @@ int64_t combine_units(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units)
     return nu;
 }
 
+// Contribution-driven ordering of the filter units (SURVEY
+// C12/C13): a unit's score is the sum of its partitions' scores (hub-driven: sum
+// of D_o*D_i over active vertices; delta-driven: sum of delta); units run in
+// descending score, ties by unit index (a stable sort of the identity order).
+void order_units(int64_t nu, const uint64_t *units, const double *part_score, uint32_t *order) {
+    std::vector<double> sc((size_t)std::max<int64_t>(nu, 0), 0.0);
+    for (int64_t j = 0; j < nu; ++j) {
+        for (uint64_t i = units[2 * j]; i < units[2 * j + 1]; ++i) sc[j] += part_score[i];
+        order[j] = (uint32_t)j;
+    }
+    std::stable_sort(order, order + nu, [&](uint32_t x, uint32_t y) { return sc[x] > sc[y]; });
+}
+
 void rank_partitions(const std::vector<uint64_t> &off, const std::vector<uint64_t> &bounds, int world, int rank,
                      uint64_t *p_lo, uint64_t *p_hi) {
     // bounds from partition_bounds_ranked: every rank cut is a partition bound
@@ -962,6 +975,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
 
     const uint64_t np = c->p_hi - c->p_lo;
     std::vector<uint8_t> pvec(np);
+    std::vector<double> pscore(np);
     std::vector<uint64_t> units(2 * np + 2);
     const uint64_t max_iters = algo == ALGO_PR ? P.max_iters : UINT64_MAX;
     uint64_t it = 0;
@@ -1038,13 +1052,11 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         std::vector<uint32_t> order((size_t)nu);
         std::iota(order.begin(), order.end(), 0u);
         if (prio != 0 && nu > 1) {
-            std::vector<double> sc((size_t)nu, 0.0);
-            for (int64_t j = 0; j < nu; ++j)
-                for (uint64_t i = units[2 * j]; i < units[2 * j + 1]; ++i) {
-                    const PartIter &pi = c->parts_h[c->p_lo + i];
-                    sc[j] += prio == 2 ? pi.dsum : (double)pi.hub;
-                }
-            std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return sc[x] > sc[y]; });
+            for (uint64_t i = 0; i < np; ++i) {
+                const PartIter &pi = c->parts_h[c->p_lo + i];
+                pscore[i] = prio == 2 ? pi.dsum : (double)pi.hub;
+            }
+            order_units(nu, units.data(), pscore.data(), order.data());
         }
         row.parts_f = (uint32_t)H.parts[ENG_F];
         row.parts_c = (uint32_t)H.parts[ENG_C];

@@ -71,8 +71,8 @@ struct Params {
     int exchange = 1;          // multi-GPU: 0 dense, 1 sparse when cheaper (§8f #3), 2 sparse when it fits,
                                // 3 fused peer push (relax writes remote destinations into their owner's memory)
     int relax_hot = 1;         // hub block in smem (PR Δ accumulation / min-algorithm value copy): 0 off, 1 auto, 2 always
-    uint64_t relax_hot_v = 8192;    // PR hub-block vertices in shared memory (8 B each: 64 KB; min-algorithms cap at kHotV)
-    int relax_threads = 512;        // relax CTA size (512: 2 CTAs/SM, 1024: 1 CTA/SM sharing a larger hub block)
+    uint64_t relax_hot_v = 16384;   // PR hub-block vertices in shared memory (8 B each: 128 KB; min-algorithms cap at kHotV)
+    int relax_threads = 0;          // relax CTA size: 0 auto (PR 1024: 1 CTA/SM sharing the hub block; else 512), 512, 1024
     int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
     uint64_t edge_cache_bytes = 0;   // cap on the cache (0 = whatever the budget leaves)
     int cpu_cost = 0;          // 1: include Eq. 2's CPU term with Thpt_cpt calibrated on this box
@@ -189,6 +189,7 @@ void release_run_ctx(hyt_graph *g);   // drop cached run buffers (parameters cha
 // host partitioner: greedy 32-MiB sweep by binary search on offsets
 std::vector<uint64_t> partition_bounds(const std::vector<uint64_t> &off, uint64_t d1, uint64_t target);
 int64_t combine_units(const uint8_t *p, uint64_t n, uint64_t k, uint64_t *units);
+void order_units(int64_t nu, const uint64_t *units, const double *part_score, uint32_t *order);
 // multi-GPU split: rank r owns vertices [R_r, R_r+1), R_r = the first vertex whose
 // edge offset reaches r*E/world (R_world = V); partitions never cross a rank cut
 void rank_vertex_range(const std::vector<uint64_t> &off, int world, int rank, uint64_t *v_lo, uint64_t *v_hi);

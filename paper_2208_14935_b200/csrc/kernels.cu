@@ -379,7 +379,9 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     A.c_lo = c_lo; A.c_hi = c_hi; A.seg_chunks = seg_chunks; A.seg_first = seg_first; A.seg_end = seg_end;
     A.dev_tot = dev_tot; A.base = src.base; A.shift = src.shift;
     if (peer) A.pp = *peer;
-    const int nt = s.relax_nt >= 1024 ? 1024 : 512;      // threads per CTA (relax_threads)
+    // threads per CTA (relax_threads; 0 = auto: PR 1024 so one CTA per SM shares a
+    // 16384-hub block, min-algorithms 512 with two CTAs per SM)
+    const int nt = s.relax_nt == 0 ? (s.algo == ALGO_PR ? 1024 : 512) : (s.relax_nt >= 1024 ? 1024 : 512);
     const uint64_t nwarps = (uint64_t)nt / 32;
     if (nt == 1024) max_ctas = (max_ctas + 1) / 2;           // same threads per SM
     uint64_t grid;

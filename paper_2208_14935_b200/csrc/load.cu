@@ -616,7 +616,10 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
     }
     HostView vn, vw;
     try {
-        vn.open(nbr, E * 4);
+        // an adopted id array is the store: register it up to its last 16-byte chunk
+        // (filter copies and chunk loads read whole chunks; the base is 16-B aligned,
+        // so the rounded end stays inside the last element's page)
+        vn.open(nbr, adopt ? ((E * 4 + 15) & ~15ull) : E * 4);
         if (w) vw.open(w, E * 4);
         HYT_REQUIRE(!adopt || !vn.tmp, HYT_ENOMEM, "HYT_ADOPT_HOST: the id array could not be registered in place");
         phase("map caller arrays");
@@ -703,7 +706,7 @@ void load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off, cons
     HostView vn, vw;
     Temps T(g->arena);
     try {
-        vn.open(nbr, n_e * 4);
+        vn.open(nbr, adopt ? ((n_e * 4 + 15) & ~15ull) : n_e * 4);
         if (w) vw.open(w, n_e * 4);
         HYT_REQUIRE(!adopt || !vn.tmp, HYT_ENOMEM, "HYT_ADOPT_HOST: the id array could not be registered in place");
         uint64_t *rs = (uint64_t *)T.get((nrows + 1) * 8 + 16, "load: row starts");

@@ -82,3 +82,19 @@ def test_binding_constants_match_header():
                                                            "host_store_bytes"]
     assert "uint64_t host_store_bytes;" in txt
     assert "uint64_t pull_iters, um_balloon_bytes;" in txt and "uint32_t dir;" in txt
+
+
+def test_order_units_matches_oracle():
+    """A5: the scheduler's contribution-driven unit order equals oracle_order_units
+    (descending unit score, ties by unit index) on random plans with many ties."""
+    import oracle
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        n = int(rng.integers(1, 60))
+        p = rng.choice([0, 1, 1, 1, 2, 3], size=n).astype(np.uint8)
+        units = hyt.combine(p, int(rng.integers(1, 6)))
+        if rng.random() < 0.5:
+            score = rng.integers(0, 4, size=n).astype(np.float64)          # integer hub sums: ties
+        else:
+            score = rng.random(n) * 10.0 ** rng.integers(-6, 3)            # delta sums
+        assert hyt.order_units(units, score) == oracle.order_units(units, score)
