@@ -214,7 +214,8 @@ int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off_ho
  *   streams [4]; engine_mode [HYT_MODE_HYBRID]; priority [-1 = auto:
  *   delta for PR, hub otherwise; 0 none, 1 hub, 2 delta];
  *   recompute [1] (process a loaded filter unit once more);
- *   damping [0.85], epsilon [1e-6], max_iters [1000] (PR);
+ *   damping [0.85], epsilon [1e-5], max_iters [1000] (PR; the per-vertex
+ *   relative truncation error is at most epsilon/(1-d) = 6.7e-5);
  *   gather_threads [0 = all cores]; compaction_buffer_bytes [0 = auto];
  *   edge_cache [0]: 1 keeps the longest hub-order prefix of partitions that fits
  *   the budget left after the run buffers resident in device memory (served as

@@ -62,7 +62,7 @@ struct Params {
     int engine_mode = MODE_HYBRID;
     int priority = -1;
     int recompute = 1;
-    double damping = 0.85, epsilon = 1e-6;
+    double damping = 0.85, epsilon = 1e-5;   // C16 (round 2): eps/(1-d) = 6.7e-5 < 1e-4
     uint64_t max_iters = 1000;
     int gather_threads = 0;
     uint64_t compaction_buffer_bytes = 0;

@@ -69,7 +69,7 @@ def test_tw_pr_residual_and_samples(tw_runs):
     g = tw()
     r, st = tw_runs["pr"]
     res = oracle.pr_residual(g.off, g.nbr, r)
-    # truncation at eps = 1e-6 leaves at most eps/(1-d) = 6.7e-6 relative (DESIGN C16)
+    # truncation at eps = 1e-5 leaves at most eps/(1-d) = 6.7e-5 relative (DESIGN C16)
     assert res["max_rel_res"] < 1e-4, res
     indeg = np.bincount(g.nbr, minlength=g.V)
     zero_in = np.nonzero(indeg == 0)[0]

@@ -5,8 +5,8 @@ with k in-flows; the north star's bar is 1e-4 max relative error per vertex).
 
   python tools/pr_error.py --config tw --shift 2 --budget-gb 2 --modes hybrid,resident
 
-For each mode: one GPU run (epsilon 1e-6), then max |r - r*| / r* over all vertices
-and per in-degree decade, r* = oracle.pr_jacobi (Jacobi to 1e-11, f64, CPU).
+For each mode: one GPU run (the library default epsilon, 1e-5), then max |r - r*| / r* over all vertices
+and per in-degree decade, r* = oracle.pr_jacobi_pull (Jacobi to 1e-11, f64, CPU threads).
 """
 import argparse
 import json
@@ -33,7 +33,7 @@ def main():
     import paper_2208_14935_b200 as hyt
     g = hytgen.make(a.config, shift=a.shift)
     t = time.time()
-    want, iters = oracle.pr_jacobi(g.off, g.nbr, tol=1e-11)
+    want, iters = oracle.pr_jacobi_pull(g.off, g.nbr, tol=1e-11)
     res = {"config": a.config, "shift": a.shift, "V": g.V, "E": g.E, "oracle_s": time.time() - t,
            "oracle_iters": iters, "rows": []}
     indeg = np.bincount(g.nbr, minlength=g.V)
