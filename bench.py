@@ -614,6 +614,17 @@ def main():
         except (OSError, ValueError, KeyError):
             traffic_ratio = {}
 
+    pattern, pattern_src = None, None
+    pf = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_scatter_bench.json")))
+    if pf:
+        try:
+            pattern = json.load(open(pf[-1]))
+            pattern_src = "profiles/" + os.path.basename(pf[-1])
+            if "uniform_l2_resident" not in pattern:
+                pattern = None
+        except (OSError, ValueError):
+            pattern = None
+
     def tag_roof(i):
         if eng_launch[i] == 0:
             return None
@@ -630,6 +641,17 @@ def main():
                   "avg_launch_ms": avg_s * 1e3, "launches": int(eng_launch[i]),
                   "share_of_kernel_time": float(eng_ms[i] / max(1e-9, eng_ms[kernel_tags].sum()))})
         r["frac"] = r["achieved"] / r["peak"]
+        if i != 3 and pattern:
+            # the same launches against the access pattern's own ceiling on this GPU:
+            # one random 4-B destination access per edge into an L2-resident array
+            # (tools/scatter_bench.cu; red.add.f32 for PR, a load for the min-algorithms)
+            ceil_red = pattern["uniform_l2_resident"]["red_add"]["gedges_s"]
+            ceil_ld = pattern["uniform_l2_resident"]["ld"]["gedges_s"]
+            eps = eng_edges[i] / eng_launch[i] / avg_s / 1e9
+            r["access_pattern"] = {"achieved_gedges_s": eps, "ceiling_red_add_gedges_s": ceil_red,
+                                   "ceiling_load_gedges_s": ceil_ld, "source": pattern_src,
+                                   "note": "random 4-B destination accesses per second; the HBM-copy frac above "
+                                           "counts them as 4 B each"}
         r["traffic"] = None
         kind = {1: "filter", 5: "filter", 4: "resident"}.get(i)
         if kind and kind in traffic_ratio:

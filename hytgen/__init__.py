@@ -156,7 +156,7 @@ def weights(g: Graph, seed: int) -> np.ndarray:
 # Workload recipes.  scale/V/E/abc/seed/symmetric.
 CONFIGS = {
     "r16": dict(scale=16, V=65_536, E=1 << 20, abc=(0.57, 0.19, 0.19), seed=16, symmetric=False),
-    "tw": dict(scale=26, V=41_700_000, E=1_470_000_000, abc=(0.57, 0.19, 0.19), seed=2, symmetric=False),
+    "tw": dict(scale=26, V=41_700_000, E=1_470_000_000, abc=(0.48, 0.21, 0.21), seed=2, symmetric=False),
     "fr": dict(scale=26, V=65_600_000, E=1_806_000_000, abc=(0.45, 0.22, 0.22), seed=3, symmetric=True),
     "uk": dict(scale=27, V=105_900_000, E=3_740_000_000, abc=(0.57, 0.19, 0.19), seed=4, symmetric=False),
     "r30": dict(scale=30, V=1 << 30, E=1 << 34, abc=(0.57, 0.19, 0.19), seed=5, symmetric=True),

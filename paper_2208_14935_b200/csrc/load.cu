@@ -67,14 +67,26 @@ void pinned_free(void *p) {
 // ---------------------------------------------------------------------------
 // kernels
 // ---------------------------------------------------------------------------
+// In-degrees from the caller's ids read in place over the link (zero-copy): 16-byte
+// loads (4 ids per lane, 512 B per warp instruction) from the first 16-byte aligned
+// id on, the unaligned head and the tail one id per thread.
 __global__ void k_indeg(const uint32_t *__restrict__ nbr, uint64_t E, uint64_t V, uint32_t *__restrict__ din,
                         uint32_t *__restrict__ bad) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < E; i += stride) {
-        const uint32_t x = nbr[i];
-        if (x >= V) { *bad = 1; continue; }
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t head = std::min<uint64_t>(E, ((16 - ((uintptr_t)nbr & 15)) & 15) / 4);
+    const uint64_t nvec = (E - head) / 4;
+    auto one = [&](uint32_t x) {
+        if (x >= V) { *bad = 1; return; }
         atomicAdd(&din[x], 1u);
+    };
+    if (tid < head) one(nbr[tid]);
+    const uint4 *v4 = reinterpret_cast<const uint4 *>(nbr + head);
+    for (uint64_t i = tid; i < nvec; i += stride) {
+        const uint4 q = v4[i];
+        one(q.x); one(q.y); one(q.z); one(q.w);
     }
+    for (uint64_t i = head + nvec * 4 + tid; i < E; i += stride) one(nbr[i]);
 }
 
 // HYT_SYMMETRIC sanity check: a symmetric edge multiset has D_i(v) = D_o(v) for
@@ -94,15 +106,26 @@ __device__ __forceinline__ uint64_t hub_key(const uint64_t *off, const uint32_t 
 
 // radix select, one 8-bit digit per pass: histogram of the digit at `shift` among
 // keys whose higher bits equal `prefix` (under `mask`)
+// One digit's histogram.  Most keys share a few digits (every vertex without in- or
+// out-edges has key 0), so lanes with equal digits are aggregated first
+// (__match_any_sync) and one lane adds the group's count: a per-key shared-memory
+// atomic on one hot bin serialised the early passes.
 __global__ void k_key_hist(const uint64_t *__restrict__ off, const uint32_t *__restrict__ din, uint64_t V,
                            uint64_t prefix, uint64_t mask, int shift, unsigned long long *__restrict__ hist) {
     __shared__ unsigned int sh[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
     __syncthreads();
+    const int lane = threadIdx.x & 31;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride) {
-        const uint64_t k = hub_key(off, din, v);
-        if ((k & mask) == prefix) atomicAdd(&sh[(k >> shift) & 0xFF], 1u);
+    const uint64_t Vr = (V + 31) & ~31ull;                   // whole warps take part in the match
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < Vr; v += stride) {
+        uint32_t digit = 256u;                               // 256: not counted
+        if (v < V) {
+            const uint64_t k = hub_key(off, din, v);
+            if ((k & mask) == prefix) digit = (uint32_t)((k >> shift) & 0xFF);
+        }
+        const uint32_t grp = __match_any_sync(FULL_MASK, digit);
+        if (digit != 256u && lane == __ffs(grp) - 1) atomicAdd(&sh[digit], (unsigned)__popc(grp));
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 256; i += blockDim.x)
