@@ -211,20 +211,49 @@ __global__ void __launch_bounds__(kItemThreads) k_plan_items(PlanArgs A) {
 // ---------------------------------------------------------------------------
 struct WarpCount { uint64_t e, c, d; };   // entries, chunks, edges
 
+// The set words of a warp's slice are visited in batches of kBatch: the offsets of
+// every lane's vertex in all words of a batch are loaded first (independent loads
+// in flight), then consumed -- one word at a time, the loads formed a chain of
+// dependent round trips that dominated the range / fill kernels.
+constexpr int kBatch = 4;
+
+__device__ __forceinline__ int next_words(uint32_t &m, int (&js)[kBatch]) {
+    int n = 0;
+#pragma unroll
+    for (int k = 0; k < kBatch; ++k) {
+        js[k] = -1;
+        if (m) { js[k] = __ffs(m) - 1; m &= m - 1; ++n; }
+    }
+    return n;
+}
+
 __device__ __forceinline__ WarpCount warp_count(const DevState &s, uint64_t ws, uint32_t myword) {
     const int lane = threadIdx.x & 31;
     WarpCount r{0, 0, 0};
     uint64_t c = 0, d = 0;
-    for (uint32_t m = __ballot_sync(FULL_MASK, myword != 0); m; m &= m - 1) {
-        const int j = __ffs(m) - 1;
-        const uint32_t bits = __shfl_sync(FULL_MASK, myword, j);
-        bool ent = false;
-        if ((bits >> lane) & 1u) {
-            const uint64_t v = ((ws + j) << 5) + lane;
-            const uint64_t o0 = s.off[v], o1 = s.off[v + 1];
-            if (o1 > o0) { ent = true; c += chunk_hi(o1, s.d1) - chunk_lo(o0, s.d1); d += o1 - o0; }
+    uint32_t m = __ballot_sync(FULL_MASK, myword != 0);
+    while (m) {
+        int js[kBatch];
+        next_words(m, js);
+        uint64_t o0[kBatch], o1[kBatch];
+        bool act[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+            const uint32_t bits = __shfl_sync(FULL_MASK, myword, js[k] < 0 ? 0 : js[k]);
+            act[k] = js[k] >= 0 && ((bits >> lane) & 1u);
+            o0[k] = o1[k] = 0;
+            if (act[k]) {
+                const uint64_t v = ((ws + js[k]) << 5) + lane;
+                o0[k] = s.off[v];
+                o1[k] = s.off[v + 1];
+            }
         }
-        r.e += __popc(__ballot_sync(FULL_MASK, ent));
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+            const bool ent = act[k] && o1[k] > o0[k];
+            if (ent) { c += chunk_hi(o1[k], s.d1) - chunk_lo(o0[k], s.d1); d += o1[k] - o0[k]; }
+            r.e += __popc(__ballot_sync(FULL_MASK, ent));
+        }
     }
     r.c = warp_sum_u64(c);
     r.d = warp_sum_u64(d);
@@ -258,32 +287,47 @@ __device__ __forceinline__ void warp_write(const DevState &s, uint64_t ws, uint3
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     uint64_t run_e = base_e, run_c = base_c;
-    for (uint32_t m = __ballot_sync(FULL_MASK, myword != 0); m; m &= m - 1) {
-        const int j = __ffs(m) - 1;
-        const uint32_t bits = __shfl_sync(FULL_MASK, myword, j);
-        const bool act = (bits >> lane) & 1u;
-        const uint64_t v = ((ws + j) << 5) + lane;
-        uint64_t o0 = 0, o1 = 0, nch = 0;
-        if (act) { o0 = s.off[v]; o1 = s.off[v + 1]; }
-        const uint64_t deg = o1 - o0;
-        const bool ent = act && deg > 0;
-        if (ent) nch = chunk_hi(o1, s.d1) - chunk_lo(o0, s.d1);
-        const uint32_t b = __ballot_sync(FULL_MASK, ent);
-        const uint64_t inc = warp_incl_u64(nch);
-        const uint64_t tot = __shfl_sync(FULL_MASK, inc, 31);
-        if (PR && TAKE_DELTA && act && deg == 0) s.rank[v] += atomicExch(&s.delta[v], 0.0f);
-        if (ent) {
-            const uint64_t idx = run_e + __popc(b & lt);
-            const uint64_t pre = run_c + inc - nch;
-            q.qv[idx] = (uint32_t)v;
-            q.qpre[idx] = pre;
-            q.qbeg[idx] = o0;
-            q.qdeg[idx] = (uint32_t)deg;
-            if (PR && !TAKE_DELTA) q.qaux[idx] = s.damping * scratch[v - v_lo] / (float)deg;
-            write_tiles(q.tile + tile_base, pre, nch, (uint32_t)idx);
+    uint32_t m = __ballot_sync(FULL_MASK, myword != 0);
+    while (m) {
+        int js[kBatch];
+        next_words(m, js);
+        uint64_t o0[kBatch], o1[kBatch];
+        bool act[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+            const uint32_t bits = __shfl_sync(FULL_MASK, myword, js[k] < 0 ? 0 : js[k]);
+            act[k] = js[k] >= 0 && ((bits >> lane) & 1u);
+            o0[k] = o1[k] = 0;
+            if (act[k]) {
+                const uint64_t v = ((ws + js[k]) << 5) + lane;
+                o0[k] = s.off[v];
+                o1[k] = s.off[v + 1];
+            }
         }
-        run_e += __popc(b);
-        run_c += tot;
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+            if (js[k] < 0) break;                          // warp-uniform
+            const uint64_t v = ((ws + js[k]) << 5) + lane;
+            const uint64_t deg = o1[k] - o0[k];
+            const bool ent = act[k] && deg > 0;
+            const uint64_t nch = ent ? chunk_hi(o1[k], s.d1) - chunk_lo(o0[k], s.d1) : 0;
+            const uint32_t b = __ballot_sync(FULL_MASK, ent);
+            const uint64_t inc = warp_incl_u64(nch);
+            const uint64_t tot = __shfl_sync(FULL_MASK, inc, 31);
+            if (PR && TAKE_DELTA && act[k] && deg == 0) s.rank[v] += atomicExch(&s.delta[v], 0.0f);
+            if (ent) {
+                const uint64_t idx = run_e + __popc(b & lt);
+                const uint64_t pre = run_c + inc - nch;
+                q.qv[idx] = (uint32_t)v;
+                q.qpre[idx] = pre;
+                q.qbeg[idx] = o0[k];
+                q.qdeg[idx] = (uint32_t)deg;
+                if (PR && !TAKE_DELTA) q.qaux[idx] = s.damping * scratch[v - v_lo] / (float)deg;
+                write_tiles(q.tile + tile_base, pre, nch, (uint32_t)idx);
+            }
+            run_e += __popc(b);
+            run_c += tot;
+        }
     }
 }
 
@@ -370,18 +414,27 @@ __global__ void __launch_bounds__(kItemThreads) k_range_count(DevState s, uint64
             if (s.bm_next[w] & m) taken = atomicAnd(&s.bm_next[w], ~m) & m;
         }
     } else {
-        for (int j = 0; j < 32; ++j) {
-            const uint64_t ww = ws + j;
-            if (ww >= whi) break;
-            const uint64_t v = (ww << 5) + lane;
-            bool act = false;
-            if (v >= v_lo && v < v_hi) act = s.delta[v] > s.epsilon;
-            const uint32_t b = __ballot_sync(FULL_MASK, act);
-            if (lane == j) taken = b;
-            if (act) {
-                const float dl = atomicExch(&s.delta[v], 0.0f);
-                s.rank[v] += dl;
-                r.scratch[v - v_lo] = dl;
+        for (int j0 = 0; j0 < 32; j0 += 8) {   // 8 words' deltas in flight per lane
+            float dl[8];
+            bool inr[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t ww = ws + j0 + u;
+                const uint64_t v = (ww << 5) + lane;
+                inr[u] = ww < whi && v >= v_lo && v < v_hi;
+                dl[u] = inr[u] ? s.delta[v] : 0.0f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint64_t v = ((ws + j0 + u) << 5) + lane;
+                const bool act = inr[u] && dl[u] > s.epsilon;
+                const uint32_t b = __ballot_sync(FULL_MASK, act);
+                if (lane == j0 + u) taken = b;
+                if (act) {
+                    const float x = atomicExch(&s.delta[v], 0.0f);
+                    s.rank[v] += x;
+                    r.scratch[v - v_lo] = x;
+                }
             }
         }
     }

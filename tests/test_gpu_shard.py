@@ -102,15 +102,15 @@ def _ranks(hyt, c, od, idg, world, algo, weighted, budget=0, engine="hybrid", pa
     return out
 
 
-def test_shard_load_world4_r30_certificates(hyt):
-    """RMAT-30 recipe at 1/128 scale (8.4M V, 134M undirected edges -> 268M stored),
+def test_shard_load_world4_r30_shift6_certificates(hyt):
+    """RMAT-30 recipe at 1/64 scale (16.8M V, 268M undirected edges -> 537M stored),
     4 in-process ranks each loading only its own rows: BFS and SSSP certificates on
     the full graph, every rank gathering all V values, and each rank's pinned store
     about 1/4 of the graph."""
-    c = hytgen.recipe("r30", 7)
+    c = hytgen.recipe("r30", 6)
     od, idg = degrees(c, world=4)
     E = int(od.astype(np.uint64).sum())
-    g = hytgen.make("r30", 7, weighted=True)       # checker side only
+    g = hytgen.make("r30", 6, weighted=True)       # checker side only
     for algo in ("bfs", "sssp"):
         outs = _ranks(hyt, c, od, idg, 4, algo, weighted=True, budget=6 << 30)
         vals = outs[0][0]
