@@ -134,6 +134,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "exchange") { integral(); in(0, 3); p.exchange = (int)v; }
         else if (k == "relax_hot") { integral(); in(0, 2); p.relax_hot = (int)v; }
         else if (k == "relax_hot_v") { integral(); in(32, 20480); p.relax_hot_v = (uint64_t)v; }
+        else if (k == "relax_bands") { integral(); in(0, 64); p.relax_bands = (int)v; }
         else if (k == "relax_threads") {
             integral();
             HYT_REQUIRE(v == 0 || v == 512 || v == 1024, HYT_EINVAL, "relax_threads must be 0 (auto), 512 or 1024");

@@ -681,6 +681,7 @@ static DevState make_state(hyt_graph *g, RunCtx *c) {
     s.epsilon = (float)g->prm.epsilon;
     s.hot_v = (uint32_t)g->prm.relax_hot_v;
     s.relax_nt = g->prm.relax_threads;
+    s.bands = (uint32_t)g->prm.relax_bands;
     return s;
 }
 
@@ -1117,7 +1118,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             cudaStream_t stm = g->st[c->S];
             EvPair e1;
             timed_begin(c, stm, e1, TAG_Z);
-            EdgeSrc es{edges_mapped, (int64_t)store_c0, false};
+            EdgeSrc es{edges_mapped, (int64_t)store_c0, false, true};
             if (algo == ALGO_PR) {
                 launch_take_delta(s, c->q, H.ent_base[ENG_Z], H.ent_base[ENG_Z] + H.ent_count[ENG_Z], stm);
                 g->launches += 1;
@@ -1155,7 +1156,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             cudaStream_t stm = g->st[0];
             EvPair e1;
             timed_begin(c, stm, e1, TAG_R);
-            EdgeSrc es{c->cache, (int64_t)c->cache_c0, false};
+            EdgeSrc es{c->cache, (int64_t)c->cache_c0, false, mode == MODE_UM};
             if (algo == ALGO_PR) {
                 launch_take_delta(s, c->q, H.ent_base[ENG_R], H.ent_base[ENG_R] + H.ent_count[ENG_R], stm);
                 g->launches += 1;

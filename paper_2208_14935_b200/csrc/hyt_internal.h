@@ -127,6 +127,7 @@ struct DevState {
     float damping, epsilon;
     uint32_t hot_v;             // hub-block size in shared memory (relax_hot_v)
     int relax_nt;               // relax CTA size: 512 or 1024 threads (relax_threads)
+    uint32_t bands;             // destination bands for device-resident edges (relax_bands; 0 = auto)
 };
 
 // Fused multi-rank push (exchange = 3): a destination outside the own range
@@ -191,6 +192,7 @@ struct EdgeSrc {
     const uint4 *base;   // chunk base pointer (device, staging slot, mapped host, compact buffer)
     int64_t shift;       // ABS: address = base + (c0(v) + j - shift)
     bool compact;        // COMPACT: address = base + (c - c_lo)
+    bool host = false;   // edges read over the link (zero-copy, managed): never re-read per band
 };
 // Relax over window [c_lo, c_hi) of the segment whose entries are [seg_first, seg_end)
 // with seg_chunks chunks; dev_tot (range queues) overrides seg_end/seg_chunks/c_hi.

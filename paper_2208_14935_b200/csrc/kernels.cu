@@ -66,6 +66,8 @@ struct RelaxArgs {
     const uint4 *base;
     int64_t shift;
     uint32_t n_hot;            // hub-block size cached in shared memory (0 = off)
+    uint32_t hot_force;        // keep the hub block however small the launch (relax_hot = 2)
+    uint32_t bands;            // destination bands (1 = one pass)
     PeerPush pp;               // fused multi-rank push (PEER instantiations only)
 };
 
@@ -165,7 +167,16 @@ k_relax(RelaxArgs A) {
         seg_chunks = A.dev_tot[1];
         c_hi = seg_chunks;
     }
-    const uint32_t n_hot = A.n_hot;
+    // The hub block costs a per-CTA init (and for PR a flush) proportional to its size:
+    // a CTA whose share of the window is small does without it (decided from the
+    // device-side totals, so recompute passes of unknown size are covered too).
+    // hot_force (relax_hot = 2, tests) keeps it whatever the size.
+    uint32_t n_hot = A.n_hot;
+    if (n_hot && !A.hot_force) {
+        const uint64_t chunks = c_hi > c_lo ? c_hi - c_lo : 0;
+        const uint64_t edges_per_cta = chunks * EPC / gridDim.x;
+        if (edges_per_cta < 2ull * n_hot) n_hot = 0;
+    }
     uint32_t *const s_lo = s_hotw, *const s_hi = s_hotw + n_hot;
     if (n_hot) {
         if (PR) {
@@ -175,7 +186,17 @@ k_relax(RelaxArgs A) {
         }
         __syncthreads();
     }
-    if (c_hi > c_lo) {
+    // Destination bands (relax_bands): with device-resident edges and a value / delta
+    // array larger than the L2, the window is swept once per band of destinations,
+    // each pass pushing only into its band (hubs in the shared-memory block are
+    // pushed in band 0), so the random destination accesses of a pass stay in an
+    // L2-sized slice.  The edges are re-read from HBM once per band (streamed,
+    // evict-first) instead of missing L2 on a random 4-byte access.
+    const uint32_t nb = A.bands ? A.bands : 1;
+    if (c_hi > c_lo)
+    for (uint32_t band = 0; band < nb; ++band) {
+        const uint32_t b_lo = (uint32_t)(S.V * band / nb), b_hi = (uint32_t)(S.V * (band + 1) / nb);
+        const uint32_t hub_cut = band == 0 ? n_hot : 0u;   // hub pushes go to smem in band 0 only
         const uint64_t ntiles_seg = (seg_chunks + kTile - 1) / kTile;
         const uint64_t t_first = c_lo / kTile, t_last = (c_hi - 1) / kTile;
         const uint64_t gw = (uint64_t)blockIdx.x * kWarps + w, nw = (uint64_t)gridDim.x * kWarps;
@@ -243,9 +264,15 @@ k_relax(RelaxArgs A) {
                     for (int qd = 0; qd < EPC; ++qd) {
                         if (qd < lo || qd >= hi) continue;
                         const uint32_t dst = words[qd];
-                        if (dst < n_hot) hub_add_fx(s_lo, s_hi, dst, xlo, xhi);
-                        else if (PEER && peer_remote(A.pp, dst)) atomicAdd(&A.pp.delta[peer_owner(A.pp, dst)][dst], x);
-                        else red_add_keep(&S.delta[dst], x, pol_keep);
+                        if (dst < n_hot) {
+                            if (dst < hub_cut) hub_add_fx(s_lo, s_hi, dst, xlo, xhi);
+                        } else if (dst < b_lo || dst >= b_hi) {
+                            // another band's destination
+                        } else if (PEER && peer_remote(A.pp, dst)) {
+                            atomicAdd(&A.pp.delta[peer_owner(A.pp, dst)][dst], x);
+                        } else {
+                            red_add_keep(&S.delta[dst], x, pol_keep);
+                        }
                     }
                 }
             } else {
@@ -270,10 +297,12 @@ k_relax(RelaxArgs A) {
                         const uint32_t words[4] = {data[r].x, data[r].y, data[r].z, data[r].w};
 #pragma unroll
                         for (int qd = 0; qd < EPC; ++qd) {
-                            const bool ok = qd >= lo && qd < hi;
                             uint32_t d, wgt = 0;
                             if (D1 == 8) { d = words[2 * qd]; wgt = words[2 * qd + 1]; }
                             else d = words[qd];
+                            // this band's destinations only (hubs: band 0)
+                            const bool ok = qd >= lo && qd < hi &&
+                                            (d < n_hot ? band == 0 : (d >= b_lo && d < b_hi));
                             uint32_t cnd;
                             if (ALGO == ALGO_BFS) cnd = src + 1u;
                             else if (ALGO == ALGO_SSSP) {
@@ -401,7 +430,25 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     // (the copy is a per-CTA load, a larger one does not pay: profiles/r01_hot_v.md)
     const uint64_t hv_cap = s.algo == ALGO_PR ? (uint64_t)s.hot_v : std::min<uint64_t>(s.hot_v, kHotV);
     const uint64_t hv = s.V < hv_cap ? s.V : hv_cap;
+    // destination bands: only for edges in device memory, and only when the array
+    // the pushes land in (4 B per vertex) exceeds three quarters of the L2
+    A.bands = 1;
+    if (!src.host) {
+        if (s.bands) A.bands = s.bands;
+        else {
+            static thread_local int l2[64] = {};
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (dev >= 0 && dev < 64 && !l2[dev] &&
+                (cudaDeviceGetAttribute(&l2[dev], cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2[dev] <= 0))
+                l2[dev] = 126 << 20;
+            const uint64_t slice = (uint64_t)(dev >= 0 && dev < 64 ? l2[dev] : (126 << 20)) * 3 / 4;
+            A.bands = (uint32_t)std::max<uint64_t>(1, (s.V * 4 + slice - 1) / slice);
+            if (A.bands > 16) A.bands = 16;
+        }
+    }
     A.n_hot = 0;
+    A.hot_force = hot == 2;
     if (hot && s.algo == ALGO_PR) A.n_hot = (uint32_t)hv;
     else if (hot == 2 || (hot == 1 && !dev_tot && (c_hi - c_lo) >= grid * nwarps * 4 * kTile)) A.n_hot = (uint32_t)hv;
     // staging of every warp + the hub block (PR: fixed-point (lo, hi) pairs)

@@ -411,3 +411,20 @@ def test_hub_block_sizes(hyt, hot_v, algo):
                 assert_pr_close(got, want)
             else:
                 assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("bands", [2, 5])
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+def test_destination_bands(hyt, bands, algo):
+    """Sweeping device-resident edges once per destination band (relax_bands) changes
+    no result, in every engine that reads device memory."""
+    for gi in (4, 9):
+        gkey = ("rmat", gi)
+        g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+        for engine in ("resident", "filter", "compaction", "hybrid"):
+            got, _, _ = run_gpu(hyt, g, algo, engine=engine, part=4096, relax_bands=bands)
+            want = expected(gkey, algo)
+            if algo == "pr":
+                assert_pr_close(got, want)
+            else:
+                assert np.array_equal(got, want)
