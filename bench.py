@@ -562,13 +562,15 @@ def main():
         # the contract's inputs live in pinned host memory: page-lock the caller's CSR
         # arrays once, outside the timed region (hyt_load_csr then reads them in place)
         pinned = pin_host(g.host_arrays())
-        e2e_ms = []
+        e2e_ms, e2e_load_s = [], []
         for _ in range(args.e2e_steps):
             barrier()
             s_ev, e_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s_ev.record(cur)
             H = new_handle()
+            tl = time.perf_counter()
             g.load(H)
+            e2e_load_s.append(time.perf_counter() - tl)
             step(H, out_bufs)
             e_ev.record(cur)
             barrier()
@@ -582,6 +584,7 @@ def main():
         h2d = sum(a.nbytes for a in g.host_arrays() if a is not None)
         unpin_host(pinned)
         e2e = {"value": edges_step / (em / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": em,
+               "load_s": float(np.mean(e2e_load_s)),
                "inputs_pinned": len(pinned) == len([a for a in g.host_arrays() if a is not None]),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * g.V * len(algos)),
                "includes": ("hyt_load_shard_begin + hyt_load_shard_rows from this rank's pinned rows" if g.shard else

@@ -72,7 +72,7 @@ struct Params {
                                // 3 fused peer push (relax writes remote destinations into their owner's memory)
     int relax_hot = 1;         // hub block in smem (PR Δ accumulation / min-algorithm value copy): 0 off, 1 auto, 2 always
     uint64_t relax_hot_v = 16384;   // PR hub-block vertices in shared memory (8 B each: 128 KB; min-algorithms cap at kHotV)
-    int relax_bands = 0;            // destination bands for device-resident edges: 0 auto (V*4 / (3/4 L2)), 1 off, n
+    int relax_bands = 1;            // destination bands for device-resident edges: 1 off (default: measured slower), 0 auto (V*4 / (3/4 L2)), n
     int relax_threads = 0;          // relax CTA size: 0 auto (PR 1024: 1 CTA/SM sharing the hub block; else 512), 512, 1024
     int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
     uint64_t edge_cache_bytes = 0;   // cap on the cache (0 = whatever the budget leaves)

@@ -501,6 +501,7 @@ static void plan_phase(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off
             prefix |= (uint64_t)d << shift;
             mask |= 0xFFull << shift;
         }
+        phase("  radix select (8 passes)");
         const uint64_t Tkey = prefix, ties = kk;      // hubs: key > T, plus `ties` of key == T by id
         k_tie_flags<<<grid_for(V), 256, 0, st>>>(off_old, din, V, Tkey, nonhub);
         exclusive_scan<uint32_t, uint32_t>(nonhub, nonhub_scan, V, stemp, st);
@@ -515,7 +516,9 @@ static void plan_phase(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off
         unsigned long long *smax = (unsigned long long *)T.get(16, "load: sort max");
         // hub ids in ascending id order, so the stable sort keeps ties by id (C11)
         k_scatter_hubs<<<grid_for(V), 256, 0, st>>>(off_old, din, V, nonhub, nonhub_scan, hid, hkey);
+        phase("  hub flags + scatter");
         sort_desc_stable(hkey, hid, hkey2, hid2, h, sflag, spos, stemp, smax, st);
+        phase("  sort the hubs");
         k_fill_u32<<<grid_for(V), 256, 0, st>>>(nonhub, V, 1u);
         k_mark_hubs<<<grid_for(h), 256, 0, st>>>(hid, h, g->new_id_d, nonhub);
         HYT_CUDA(cudaStreamSynchronize(st));
@@ -528,7 +531,9 @@ static void plan_phase(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off
     k_finish_perm<<<grid_for(V), 256, 0, st>>>(V, h, nonhub, nonhub_scan, off_old, din, g->new_id_d,
                                               g->old_of_d, deg2, g->din_d);
     exclusive_scan<uint64_t, uint64_t>(deg2, g->off_d, V + 1, stemp, st);
+    phase("  permutation + new offsets");
     g->off_h.resize(V + 1);
+    phase("  host offsets allocation");
     HYT_CUDA(copy_sync(g->off_h.data(), g->off_d, (V + 1) * 8, st));
     HYT_REQUIRE(g->off_h[V] == E, HYT_ESTATE, "internal: permuted offsets do not sum to E");
     rank_vertex_range(g->off_h, g->world, g->rank, &g->store_v_lo, &g->store_v_hi);
