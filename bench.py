@@ -677,7 +677,7 @@ def main():
         extras = run_extras(hyt, local, tw_graph=g.g)
 
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N = 1 only
         try:
             native = use_native_oracle()
             cpu = cpu_oracle_sample(args.config, max(args.shift, args.cpu_shift), algos)

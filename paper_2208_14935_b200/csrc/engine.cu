@@ -433,6 +433,23 @@ static void build_pull_slices(hyt_graph *g, RunCtx *c) {
     HYT_CUDA(copy_sync(c->hs_e1, e1.data(), c->n_hs * 8, g->main));
 }
 
+// Grow the pinned host copy of the compaction queue to at least n entries (called
+// between iterations, when nothing reads the old arrays).
+static void ensure_cq(RunCtx *c, uint64_t n) {
+    if (n <= c->cq_cap) return;
+    const uint64_t cap = std::min<uint64_t>(c->q.cap, std::max<uint64_t>(n, 2 * c->cq_cap));
+    for (void *old : {(void *)c->cq_v, (void *)c->cq_pre}) {
+        c->pinned.erase(std::find(c->pinned.begin(), c->pinned.end(), old));
+        pinned_free(old);
+    }
+    c->cq_v = nullptr;
+    c->cq_pre = nullptr;
+    c->cq_cap = 0;
+    c->cq_v = halloc<uint32_t>(c, cap);
+    c->cq_pre = halloc<uint64_t>(c, cap);
+    c->cq_cap = cap;
+}
+
 static RunCtx *build_ctx(hyt_graph *g, int algo) {
     const Params &P = g->prm;
     RunCtx *c = new RunCtx();
@@ -595,7 +612,9 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 c->hstage[i] = halloc<uint4>(c, cb / 16);
                 HYT_CUDA(cudaEventCreateWithFlags(&c->ev_cbuf[i], cudaEventDisableTiming));
             }
-            c->cq_cap = c->q.cap;
+            // host copy of the C queue: grown on demand (ensure_cq); the first 64K
+            // entries also serve the Thpt_cpt probe
+            c->cq_cap = std::min<uint64_t>(c->q.cap, 1ull << 16);
             c->cq_v = halloc<uint32_t>(c, c->cq_cap);
             c->cq_pre = halloc<uint64_t>(c, c->cq_cap);
             unsigned nt = P.gather_threads > 0 ? (unsigned)P.gather_threads
@@ -1068,6 +1087,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         // C queue to the host (needed by the gather) -- enqueued before the GPU work
         const uint64_t nC = H.ent_count[ENG_C];
         if (nC) {
+            ensure_cq(c, nC);
             HYT_CUDA(cudaMemcpyAsync(c->cq_v, c->q.qv + H.ent_base[ENG_C], nC * 4, cudaMemcpyDeviceToHost, main));
             HYT_CUDA(cudaMemcpyAsync(c->cq_pre, c->q.qpre + H.ent_base[ENG_C], nC * 8, cudaMemcpyDeviceToHost, main));
         }

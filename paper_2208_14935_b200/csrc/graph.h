@@ -145,6 +145,7 @@ struct hyt_graph {
     const void *adopt_key = nullptr, *adopt_dev = nullptr;
     // ---- two-phase (shard) load state ----
     bool planned = false;           // hyt_load_shard_begin done, rows not yet loaded
+    bool off_h_pending = false;     // off_h not yet copied back (one rank: fetched during the relabel)
     uint32_t ld_flags = 0;
     uint64_t *ld_off_old = nullptr; // device: caller offsets (original order), until the rows are loaded
     // ---- streams ----

@@ -260,6 +260,13 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
     }
 }
 
+// Offsets must be non-decreasing (the O(1) end checks run on the host).
+__global__ void k_check_offsets(const uint64_t *__restrict__ off, uint64_t V, uint32_t *__restrict__ bad) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t v = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; v < V; v += stride)
+        if (off[v] > off[v + 1]) *bad = 3;
+}
+
 __global__ void k_u32_to_u64(const uint32_t *__restrict__ in, uint64_t n, uint64_t *__restrict__ out) {
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) out[i] = in[i];
@@ -421,6 +428,14 @@ static uint32_t read_flag(uint32_t *bad, cudaStream_t st) {
     return h;
 }
 
+// Host copy of the internal offsets (partitioning, filter spans, host gathers).
+static void fetch_host_offsets(hyt_graph *g, cudaStream_t st) {
+    g->off_h.resize(g->V + 1);
+    HYT_CUDA(copy_sync(g->off_h.data(), g->off_d, (g->V + 1) * 8, st));
+    HYT_REQUIRE(g->off_h[g->V] == g->E, HYT_ESTATE, "internal: permuted offsets do not sum to E");
+    g->off_h_pending = false;
+}
+
 // off_host: caller offsets u64[V+1] (full CSR), or out_deg u32[V] (shard);
 // in_deg u32[V] or null (then nbr_dev, the caller's full ids mapped, is counted).
 static void plan_phase(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off_host, const uint32_t *out_deg,
@@ -444,6 +459,8 @@ static void plan_phase(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off
     HYT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
     if (off_host) {
         HYT_CUDA(cudaMemcpyAsync(off_old, off_host, (V + 1) * 8, cudaMemcpyHostToDevice, st));
+        k_check_offsets<<<grid_for(V), 256, 0, st>>>(off_old, V, bad);
+        HYT_REQUIRE(read_flag(bad, st) == 0, HYT_EINVAL, "offsets not non-decreasing");
     } else {   // offsets = exclusive scan of the out-degrees (V+1 items, the last 0)
         uint32_t *od = (uint32_t *)T.get((V + 1) * 4 + 16, "load: out-degrees");
         HYT_CUDA(cudaMemcpyAsync(od, out_deg, V * 4, cudaMemcpyHostToDevice, st));
@@ -532,11 +549,17 @@ static void plan_phase(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off
                                               g->old_of_d, deg2, g->din_d);
     exclusive_scan<uint64_t, uint64_t>(deg2, g->off_d, V + 1, stemp, st);
     phase("  permutation + new offsets");
-    g->off_h.resize(V + 1);
-    phase("  host offsets allocation");
-    HYT_CUDA(copy_sync(g->off_h.data(), g->off_d, (V + 1) * 8, st));
-    HYT_REQUIRE(g->off_h[V] == E, HYT_ESTATE, "internal: permuted offsets do not sum to E");
-    rank_vertex_range(g->off_h, g->world, g->rank, &g->store_v_lo, &g->store_v_hi);
+    if (g->world == 1 && off_host) {
+        // one rank serves every edge: the store range is known without the host copy
+        // of the offsets, which rows_phase fetches while the relabel runs
+        HYT_CUDA(cudaStreamSynchronize(st));
+        g->store_v_lo = 0;
+        g->store_v_hi = V;
+        g->off_h_pending = true;
+    } else {
+        fetch_host_offsets(g, st);
+        rank_vertex_range(g->off_h, g->world, g->rank, &g->store_v_lo, &g->store_v_hi);
+    }
     phase("hub sort + new offsets");
 }
 
@@ -550,7 +573,8 @@ static void rows_phase(hyt_graph *g, const uint64_t *row_start, const uint32_t *
     cudaStream_t st = g->main;
     const uint64_t V = g->V;
     g->weighted = weighted;
-    const uint64_t e_lo = g->off_h[g->store_v_lo], e_hi = g->off_h[g->store_v_hi];
+    const uint64_t e_lo = g->off_h_pending ? 0 : g->off_h[g->store_v_lo];
+    const uint64_t e_hi = g->off_h_pending ? g->E : g->off_h[g->store_v_hi];
     g->store_c0[0] = e_lo / 4;                          // first chunk of u32 ids
     g->store_c0[1] = e_lo / 2;                          // first chunk of u64 records
     const uint64_t nbase = g->store_c0[0] * 4, wbase = g->store_c0[1] * 2;
@@ -587,6 +611,17 @@ static void rows_phase(hyt_graph *g, const uint64_t *row_start, const uint32_t *
                                                       nbr_out ? nbr_out - nbase : nullptr,
                                                       ew_out ? ew_out - wbase : nullptr, bad);
     }
+    if (g->off_h_pending) {   // the host offsets while the relabel kernel runs (its own stream)
+        cudaStream_t side = nullptr;
+        HYT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        try {
+            fetch_host_offsets(g, side);
+        } catch (...) {
+            cudaStreamDestroy(side);
+            throw;
+        }
+        cudaStreamDestroy(side);
+    }
     HYT_REQUIRE(read_flag(bad, st) == 0, HYT_EINVAL, "neighbour id >= V");
     HYT_CUDA(cudaGetLastError());
     phase("relabel edges (zero-copy)");
@@ -601,6 +636,7 @@ static void load_done(hyt_graph *g) {
 
 static void load_fail(hyt_graph *g) {
     cudaStreamSynchronize(g->main);
+    g->off_h_pending = false;
     if (g->ld_off_old) g->arena.release(g->ld_off_old);
     g->ld_off_old = nullptr;
     g->planned = false;
@@ -609,8 +645,7 @@ static void load_fail(hyt_graph *g) {
 static void check_offsets(const uint64_t *off, uint64_t V, uint64_t E) {
     HYT_REQUIRE(off[0] == 0, HYT_EINVAL, "off[0] != 0");
     HYT_REQUIRE(off[V] == E, HYT_EINVAL, "off[V] != E");
-    for (uint64_t v = 0; v < V; ++v)
-        HYT_REQUIRE(off[v] <= off[v + 1], HYT_EINVAL, "offsets not non-decreasing at " + std::to_string(v));
+    // monotonicity is checked on the GPU (k_check_offsets) once the offsets are there
 }
 
 void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const uint32_t *nbr,
@@ -654,9 +689,10 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         plan_phase(g, V, E, off, nullptr, nullptr, (const uint32_t *)vn.dev, flags, phase);
         const uint32_t *adopt_ids = nullptr;
         if (adopt) {
-            HYT_REQUIRE(g->off_h[g->store_v_lo] % 4 == 0, HYT_EINVAL,
+            const uint64_t first = g->off_h_pending ? 0 : g->off_h[g->store_v_lo];
+            HYT_REQUIRE(first % 4 == 0, HYT_EINVAL,
                         "HYT_ADOPT_HOST: this rank's first edge is not on a 16-byte chunk boundary");
-            adopt_ids = nbr + g->off_h[g->store_v_lo];
+            adopt_ids = nbr + first;
         }
         rows_phase(g, nullptr, (const uint32_t *)vn.dev, (const uint32_t *)vw.dev, w != nullptr, &early, adopt_ids,
                    phase);

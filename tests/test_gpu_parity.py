@@ -293,6 +293,14 @@ def test_errors(hyt):
         with pytest.raises(hyt.HytError) as ei:
             G.load(g.off, bad, g.w)
         assert ei.value.code == hyt.HYT_EINVAL
+        off = g.off.copy(); k = len(off) // 2; off[k] = off[k + 1] + 1     # not non-decreasing
+        G3 = hyt.Graph(device=0)
+        try:
+            with pytest.raises(hyt.HytError) as ei:
+                G3.load(off, g.nbr, g.w)
+            assert ei.value.code == hyt.HYT_EINVAL and "non-decreasing" in str(ei.value)
+        finally:
+            G3.close()
         G2 = hyt.Graph(device=0)
         G2.load(g.off, g.nbr, None)
         with pytest.raises(hyt.HytError) as ei:

@@ -66,7 +66,7 @@ def main():
         out["rows"][setting] = {"summary": summ, "runs": rows}
         print(setting, json.dumps(summ), flush=True)
         for k in kv:   # back to defaults
-            G.set(k, {"cost_model": 1, "epsilon": 1e-5}.get(k, 0))
+            G.set(k, {"cost_model": 1, "epsilon": 1e-5, "zc_weight": 1.0, "relax_bands": 1}.get(k, 0))
     G.close()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
