@@ -15,9 +15,23 @@ in pinned host memory, offsets/vertex state in HBM).  value = whole-job GTEPS =
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--config tw] [--shift S] [--budget-gb 16] [--algos sssp,pr]
 
-For N > 1 launch with torchrun (one rank per GPU, NCCL): every rank loads the
-graph, serves its contiguous range of partitions and the ranks reduce the pushed
-values once per iteration.  Rank 0 prints ONE JSON line.
+For N > 1 launch with torchrun (one rank per GPU, NCCL): every rank counts the
+degrees of its slice of edge indices, the ranks all-reduce them, and each rank
+loads only the rows it serves (the two-phase shard load, include/hyt.h), serves its
+contiguous range of partitions, and the ranks reduce the pushed values once per
+iteration.  Rank 0 prints ONE JSON line.
+
+Besides the contract's keys the line carries (N = 1):
+  extras        one timed run per (config, algorithm, engine mode) after a warm-up:
+                R16 resident / hybrid with the oracle's time, TW at 16 GB, FR at 4 GB,
+                UK at 8 GB, each in hybrid, filter, zero-copy and (not PR) compaction,
+                with transfer / edge volume (Table V / VI analogs);
+  cpu_baseline  the oracle built -O3 -march=native on this host, on tw>>6 and a
+                full-size Dijkstra on TW, with the host's CPU model and cores;
+  roofline      the dominant kernel against the HBM copy peak (the contract) and
+                against its access pattern's ceiling (profiles/r02_scatter_bench.json);
+  kernels / host_link / engine_ms / per_algo  the rest of the breakdown.
+--no-extras / --no-cpu-baseline / --no-cpu-full shorten a run.
 """
 from __future__ import annotations
 

@@ -361,7 +361,16 @@ int hyt_init_dist_local(hyt_graph *g, int rank, int world, uint64_t group);
 int64_t hyt_rank_range(const uint64_t *off_host, uint64_t V, uint64_t d1, uint64_t partition_bytes, int world,
                        int rank, uint64_t *p_lo, uint64_t *p_hi, uint64_t *v_lo, uint64_t *v_hi);
 
-/* Release everything (device arena, pinned host memory, streams, NCCL). */
+/* Pinned host memory the library frees (edge stores, staging) stays registered in
+ * a process-wide cache and is reused by the next allocation it fits (a new handle's
+ * store, a run context's buffers), because pinning costs about a second per 15 GB.
+ * The cache holds at most HYT_PIN_CACHE_GB GiB (environment, default 32; 0 turns
+ * it off).  hyt_trim_pinned_cache returns every cached block to the OS.  Needs no
+ * handle; thread-safe. */
+void hyt_trim_pinned_cache(void);
+
+/* Release everything (device arena, pinned host memory -- into the pinned cache --,
+ * streams, NCCL). */
 void hyt_free(hyt_graph *g);
 
 /* Thread-local message of this thread's last failure ("" if none). */

@@ -86,6 +86,7 @@ _SIGS = {
     "hyt_init_dist": ([_vp, _i32, _i32, _vp], _i32),
     "hyt_init_dist_local": ([_vp, _i32, _i32, _u64], _i32),
     "hyt_free": ([_vp], None),
+    "hyt_trim_pinned_cache": ([], None),
     "hyt_last_error": ([], ctypes.c_char_p),
     "hyt_version": ([], ctypes.c_char_p),
 }

@@ -29,6 +29,8 @@ using namespace hyt;
 
 extern "C" {
 
+void hyt_trim_pinned_cache(void) { pinned_trim(); }
+
 const char *hyt_version(void) { return "hyt-b200 0.1 (sm_100a)"; }
 const char *hyt_last_error(void) { return get_error(); }
 

@@ -97,7 +97,8 @@ CostParams make_cost(const Params &p, uint32_t d1, double cpu_ratio = 0.0, doubl
 // touch + cudaHostRegister.  About 9x faster to create than cudaHostAlloc on the
 // B200 box (tools/pin_bench.cu: 0.34 s vs 3.1 s for 8 GB).
 void *pinned_alloc(uint64_t bytes);
-void pinned_free(void *p);
+void pinned_free(void *p);     // keeps the block registered in a bounded cache (HYT_PIN_CACHE_GB)
+void pinned_trim();            // release every cached block
 
 // Every host<->device copy and memset runs on one of the library's (non-blocking)
 // streams.  A synchronous cudaMemcpy from pageable memory goes through the legacy

@@ -24,14 +24,52 @@ namespace hyt {
 static std::mutex g_pin_mu;
 static std::unordered_map<void *, uint64_t> g_pinned;
 
+// Pinning is expensive (first touch of every page + cudaHostRegister: about 1.3 s for
+// TW's 17.6 GB store on the pool's 16-core hosts, and the registration holds the
+// driver while it runs), so freed blocks are kept, still registered, and handed to
+// the next allocation that fits (a new handle's edge store, a run context's staging):
+// a caching host allocator like the device-side ones.  Bounded by HYT_PIN_CACHE_GB
+// (default 32 GiB; 0 disables it); hyt_trim_pinned_cache() returns everything.
+struct PinBlock { void *p; uint64_t len; };
+static std::vector<PinBlock> g_pin_cache;
+static uint64_t g_pin_cached = 0;
+
+static uint64_t pin_cache_cap() {
+    static uint64_t cap = [] {
+        const char *e = getenv("HYT_PIN_CACHE_GB");
+        const double gb = e ? atof(e) : 32.0;
+        return (uint64_t)(gb > 0 ? gb * (double)(1ull << 30) : 0.0);
+    }();
+    return cap;
+}
+
 void *pinned_alloc(uint64_t bytes) {
     const uint64_t huge = 2ull << 20;
     const uint64_t len = (bytes + huge - 1) / huge * huge;
+    {   // a cached block of at least len and at most 5/4 of it (contents are not zeroed:
+        // every user writes what it reads; the edge store's padding is never interpreted)
+        std::lock_guard<std::mutex> l(g_pin_mu);
+        int best = -1;
+        for (int i = 0; i < (int)g_pin_cache.size(); ++i) {
+            const uint64_t L = g_pin_cache[i].len;
+            if (L >= len && L <= len + len / 4 && (best < 0 || L < g_pin_cache[best].len)) best = i;
+        }
+        if (best >= 0) {
+            PinBlock b = g_pin_cache[best];
+            g_pin_cache.erase(g_pin_cache.begin() + best);
+            g_pin_cached -= b.len;
+            g_pinned[b.p] = b.len;
+            return b.p;
+        }
+    }
     void *p = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
     if (p == MAP_FAILED) throw Err{HYT_ENOMEM, "mmap of " + std::to_string(len) + " B failed"};
     madvise(p, len, MADV_HUGEPAGE);
-    // parallel first touch (the registration pins resident pages)
-    unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    // parallel first touch (the registration pins resident pages); two cores stay free
+    // for the thread that drives the GPU meanwhile (the load pins its store while the
+    // GPU hub-sorts)
+    const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+    unsigned nt = std::max(1u, std::min(16u, hc > 4 ? hc - 2 : hc));
     if (len < (256ull << 20)) nt = 1;
     std::vector<std::thread> th;
     for (unsigned t = 0; t < nt; ++t) {
@@ -50,18 +88,45 @@ void *pinned_alloc(uint64_t bytes) {
     return p;
 }
 
+static void pin_release(void *p, uint64_t len) {
+    cudaHostUnregister(p);
+    munmap(p, len);
+}
+
 void pinned_free(void *p) {
     if (!p) return;
     uint64_t len = 0;
+    std::vector<PinBlock> evict;
     {
         std::lock_guard<std::mutex> l(g_pin_mu);
         auto it = g_pinned.find(p);
         if (it == g_pinned.end()) return;
         len = it->second;
         g_pinned.erase(it);
+        const uint64_t cap = pin_cache_cap();
+        if (len <= cap) {   // keep it; evict the oldest blocks beyond the cap
+            g_pin_cache.push_back({p, len});
+            g_pin_cached += len;
+            while (g_pin_cached > cap) {
+                evict.push_back(g_pin_cache.front());
+                g_pin_cached -= g_pin_cache.front().len;
+                g_pin_cache.erase(g_pin_cache.begin());
+            }
+            p = nullptr;
+        }
     }
-    cudaHostUnregister(p);
-    munmap(p, len);
+    for (auto &b : evict) pin_release(b.p, b.len);
+    if (p) pin_release(p, len);
+}
+
+void pinned_trim() {
+    std::vector<PinBlock> all;
+    {
+        std::lock_guard<std::mutex> l(g_pin_mu);
+        all.swap(g_pin_cache);
+        g_pin_cached = 0;
+    }
+    for (auto &b : all) pin_release(b.p, b.len);
 }
 
 // ---------------------------------------------------------------------------
