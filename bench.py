@@ -73,6 +73,9 @@ def parse():
     ap.add_argument("--cpu-shift", type=int, default=6, help="oracle sample = the workload >> cpu_shift")
     ap.add_argument("--json-out", default="")
     ap.add_argument("--detail-out", default="", help="write per-iteration logs + stats of the last step here")
+    ap.add_argument("--dist", action="store_true",
+                    help="take the multi-rank path even at N = 1 (NCCL communicator, shard load, per-iteration "
+                         "exchange; every collective is an identity at world 1)")
     ap.add_argument("--set", action="append", default=[], help="extra library parameter key=value (experiments)")
     return ap.parse_args()
 
@@ -155,13 +158,13 @@ class Workload:
     rows the rank serves and the rank regenerates only those (hytgen.rmat_rows), so
     no process holds the whole graph (BASELINE configs[4])."""
 
-    def __init__(self, config, shift, weighted, world=1, rank=0, local=0):
+    def __init__(self, config, shift, weighted, world=1, rank=0, local=0, shard=False):
         import hytgen
         t = time.time()
         self.c = hytgen.recipe(config, shift)
         self.weighted, self.world, self.rank = weighted, world, rank
         self.V, self.symmetric = self.c["V"], bool(self.c["symmetric"])
-        self.shard = world > 1
+        self.shard = shard
         self.g = None
         self.rows = self.loff = self.lnbr = self.lw = None
         if not self.shard:
@@ -460,7 +463,12 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    multi = world > 1 or args.dist
+    if multi:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     algos = args.algos.split(",")
     budget = int(args.budget_gb * (1 << 30))
@@ -468,12 +476,12 @@ def main():
     # ---- inputs (host), generation not timed ----
     if world > 1:
         os.environ.setdefault("HYTGEN_THREADS", str(max(1, (os.cpu_count() or 8) // world)))
-    g = Workload(args.config, args.shift, True, world, rank, local)
+    g = Workload(args.config, args.shift, True, world, rank, local, shard=multi)
     dstats = g.degree_stats()
 
     def new_handle():
         G = hyt.Graph(device=local, budget=budget)
-        if world > 1:
+        if multi:
             uid = [hyt.nccl_unique_id() if rank == 0 else None]
             dist.broadcast_object_list(uid, src=0)
             G.init_dist(rank, world, uid[0])
@@ -490,7 +498,7 @@ def main():
     gen_s = g.gen_s
 
     def barrier():
-        if world > 1:
+        if multi:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -562,7 +570,7 @@ def main():
                 tot += ms
             times.append(tot)
     step_ms = float(np.mean(times))
-    if world > 1:
+    if multi:
         tt = torch.tensor([step_ms], device=f"cuda:{local}")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         step_ms = float(tt.item())
@@ -591,7 +599,7 @@ def main():
             e2e_ms.append(s_ev.elapsed_time(e_ev))
             H.close()
         em = float(np.mean(e2e_ms))
-        if world > 1:
+        if multi:
             tt = torch.tensor([em], device=f"cuda:{local}")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             em = float(tt.item())
@@ -609,7 +617,7 @@ def main():
         G.close()
 
     if rank != 0:
-        if world > 1:
+        if multi:
             dist.barrier()
             dist.destroy_process_group()
         return 0
@@ -687,11 +695,13 @@ def main():
                  "note": "algorithmic host-link bytes (filter spans + compacted chunks + zero-copy lines) / step time"}
 
     extras = None
-    if world == 1 and not args.no_extras and args.shift == 0 and args.config == "tw":
+    if not multi and not args.no_extras and args.shift == 0 and args.config == "tw":
         extras = run_extras(hyt, local, tw_graph=g.g)
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:   # the contract: rank 0 at N = 1 only
+        if multi:
+            args.no_cpu_full = True                   # the sharded workload holds no full CSR
         try:
             native = use_native_oracle()
             cpu = cpu_oracle_sample(args.config, max(args.shift, args.cpu_shift), algos)
@@ -708,7 +718,7 @@ def main():
                        "runs_s": [x / 1e3 for x in per_algo_ms[a]],
                        "gteps": edges_per[a] / (ms / 1e3) / 1e9,
                        "edges": int(edges_per[a]), "iterations": int(iters[a])}
-        if world > 1:
+        if multi:
             per_algo[a]["exchange"] = exch[a]
     line = {
         "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
@@ -717,9 +727,9 @@ def main():
         "config": {"workload": workload_desc(args.config, args.shift, algos),
                    "budget_gb": args.budget_gb, "engine_mode": args.engine, "partition_bytes": 32 << 20,
                    "params": args.set,
-                   "cost_model": "calibrated on this box (SURVEY §8f #2; cost_model=0 is the paper's PCIe-3 rule)",
+                   "cost_model": "cost_model=1: calibrated on this box for SSSP/BFS/CC, the paper's PCIe-3 rule for PR (SURVEY §8f #2)",
                    "calibration": calib,
-                   "parallelism": f"vertex-range x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"vertex-range x{world}" + (" (NCCL)" if multi else "")) if multi else "single GPU",
                    "l2": L2_NOTE, "degree_stats": dstats},
         "per_algo": per_algo,
         "roofline": roof,
@@ -741,7 +751,7 @@ def main():
     if args.json_out:
         with open(args.json_out, "w") as f:
             f.write(s + "\n")
-    if world > 1:
+    if multi:
         dist.barrier()
         dist.destroy_process_group()
     return 0

@@ -226,8 +226,10 @@ int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off_ho
  *   link rate and Thpt_cpt calibrated on this box (or set by link_gbs /
  *   thpt_cpt_gbs); the paper omits the term in selection, so 0 is the
  *   paper's rule; zc_weight [1.0] multiplies Tiz (Eq. 3)
- *   before the comparisons (1 = the paper); cost_model [1]: 1 replaces the
- *   PCIe-3 constants by costs measured on this box -- Eq. 2's CPU term as with
+ *   before the comparisons (1 = the paper); cost_model [1]: 2 replaces the
+ *   PCIe-3 constants by costs measured on this box for every algorithm, 1 does so
+ *   for BFS / SSSP / CC and keeps the paper's constants for delta-PR (measured
+ *   1-2 % faster there: the rule has no term for a filter unit's recompute pass) -- Eq. 2's CPU term as with
  *   cpu_cost, and Eq. 3 as (active lists x random-request time + further lines
  *   x streamed-line time) / RTT, probed once per process on a pinned buffer
  *   (zc_req_ns / zc_line_ns / link_gbs / thpt_cpt_gbs override the probes;

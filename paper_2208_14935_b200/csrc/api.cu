@@ -146,7 +146,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "edge_cache_bytes") { integral(); in(0, 1e13); p.edge_cache_bytes = (uint64_t)v; }
         else if (k == "cpu_cost") { integral(); in(0, 1); p.cpu_cost = (int)v; }
         else if (k == "zc_weight") { in(0.001, 1000); p.zc_weight = v; }
-        else if (k == "cost_model") { integral(); in(0, 1); p.cost_model = (int)v; }
+        else if (k == "cost_model") { integral(); in(0, 2); p.cost_model = (int)v; }
         else if (k == "zc_req_ns") { in(0, 1e6); p.zc_req_ns = v; g->est_zc_req_ns = v; }
         else if (k == "zc_line_ns") { in(0, 1e6); p.zc_line_ns = v; g->est_zc_line_ns = v; }
         else if (k == "cal_probe_bytes") { integral(); in(256.0 * (1 << 20), 1e12); p.cal_probe_bytes = (uint64_t)v; }

@@ -206,18 +206,20 @@ void dist_init_local(hyt_graph *g, int rank, int world, uint64_t group) {
     g->world = world;
     g->local_group = sp.get();
     g->local_key = group;
+    g->multi = true;
 }
 
 void dist_init(hyt_graph *g, int rank, int world, const void *uid) {
     g->rank = rank;
     g->world = world;
-    if (world == 1) return;
+    // a one-rank communicator too: the job's transport is the same at every world size
     nccl_uid_t id;
     std::memcpy(&id, uid, sizeof(id));
     HYT_CUDA(cudaSetDevice(g->device));
     nccl_comm_t comm = nullptr;
     HYT_NCCL(nccl().CommInitRank(&comm, world, id, rank));
     g->nccl_comm = comm;
+    g->multi = true;
 }
 
 void dist_allreduce_min_u32(hyt_graph *g, uint32_t *buf, uint64_t n, cudaStream_t st) {

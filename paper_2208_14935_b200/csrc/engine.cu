@@ -466,9 +466,9 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->red = dalloc<uint64_t>(g, c, 2, "reduction scratch");
         c->racc = dalloc<uint64_t>(g, c, 4, "recompute statistics");
         c->outbuf = dalloc<uint32_t>(g, c, V, "result staging");
-        if (g->world > 1 && algo != ALGO_PR)
+        if (g->multi && algo != ALGO_PR)
             c->snap = dalloc<uint32_t>(g, c, c->v_hi - c->v_lo + 1, "exchange snapshot");
-        if (g->world > 1 && P.exchange && P.exchange != 3) {
+        if (g->multi && P.exchange && P.exchange != 3) {
             // sparse pays only below V*4 / (8 * world) pairs per rank: size for that
             c->xcap = V / (2 * (uint64_t)g->world) + 1;
             c->xsend = dalloc<uint2>(g, c, c->xcap, "exchange pairs (own)");
@@ -635,10 +635,10 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         }
         // CC pulls neighbours' labels: across ranks only with an exchange that leaves
         // every rank's copy current (dense / sparse), not with the peer push
-        const bool cc_pull = algo == ALGO_CC && (g->world == 1 || P.exchange != 3);
+        const bool cc_pull = algo == ALGO_CC && (!g->multi || P.exchange != 3);
         if (P.direction && g->symmetric && (algo == ALGO_BFS || cc_pull) && c->cache && c->cache_hi == c->p_hi) {
             build_pull_slices(g, c);
-            if (g->world > 1) c->bm_glob = dalloc<uint32_t>(g, c, W + 2, "global frontier");
+            if (g->multi) c->bm_glob = dalloc<uint32_t>(g, c, W + 2, "global frontier");
         }
         // streams
         const int nst = std::max(c->S, 1) + 2;
@@ -858,12 +858,20 @@ static void calibrate(hyt_graph *g, RunCtx *c) {
     }
 }
 
-static CostParams cost_for(hyt_graph *g, uint32_t d1) {
+// cost_model 1 calibrates the rule for the min-algorithms (BFS / SSSP / CC) and keeps
+// the paper's constants for delta-PR; 2 calibrates every algorithm.  The per-iteration
+// rule has no term for the recompute pass a filter unit gets (A6): for an
+// accumulative algorithm that pass is worth a second relaxation of the unit's
+// reactivated vertices, and the calibrated rule, which sends more late partitions to
+// zero-copy, was measured 1-2 % slower than the paper's on TW and UK PR
+// (profiles/r02_pr_zcw_{tw,uk}.json), where it is 14-19 % faster on SSSP / BFS.
+static CostParams cost_for(hyt_graph *g, uint32_t d1, int algo) {
     const Params &P = g->prm;
+    const bool cal = P.cost_model == 2 || (P.cost_model == 1 && algo != ALGO_PR);
     double ratio = 0.0, zr = 0.0, zs = 0.0;
-    if ((P.cpu_cost || P.cost_model) && g->est_link_gbs > 0 && g->est_cpt_gbs > 0)
+    if ((P.cpu_cost || cal) && g->est_link_gbs > 0 && g->est_cpt_gbs > 0)
         ratio = g->est_link_gbs / g->est_cpt_gbs;
-    if (P.cost_model && g->est_link_gbs > 0 && g->est_zc_req_ns > 0) {
+    if (cal && g->est_link_gbs > 0 && g->est_zc_req_ns > 0) {
         // RTT = the time of one saturated TLP (m * MR bytes) at the DMA link rate
         const double rtt_ns = (double)(P.m * P.mr) / g->est_link_gbs;
         zr = g->est_zc_req_ns / rtt_ns;
@@ -888,7 +896,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     DevState s = make_state(g, c);
     cudaStream_t main = g->main;
     calibrate(g, c);
-    const CostParams cp = cost_for(g, c->d1);
+    const CostParams cp = cost_for(g, c->d1, algo);
     const int mode = P.engine_mode;
     const int prio = P.priority >= 0 ? P.priority : (algo == ALGO_PR ? 2 : 1);
     const int sms = num_sms();
@@ -930,10 +938,10 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             }
         }
     }
-    const bool cc_pull = algo == ALGO_CC && (g->world == 1 || P.exchange != 3);
+    const bool cc_pull = algo == ALGO_CC && (!g->multi || P.exchange != 3);
     bool pull_ok = P.direction && g->symmetric && (algo == ALGO_BFS || cc_pull) && c->cache &&
-                   c->cache_hi == c->p_hi && c->d1 == 4 && (g->world == 1 || c->bm_glob);
-    if (g->world > 1 && P.direction && g->symmetric && (algo == ALGO_BFS || cc_pull)) {
+                   c->cache_hi == c->p_hi && c->d1 == 4 && (!g->multi || c->bm_glob);
+    if (g->multi && P.direction && g->symmetric && (algo == ALGO_BFS || cc_pull)) {
         // every rank must take the same branch (the pull gathers the frontier): AND over ranks
         uint32_t f = pull_ok ? 1u : 0u;
         HYT_CUDA(cudaMemcpyAsync(c->red, &f, 4, cudaMemcpyHostToDevice, main));
@@ -956,7 +964,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     }
     launch_init_values(s, src_int, g->old_of_d, main);
     HYT_CUDA(cudaGetLastError());
-    if (g->world > 1 && algo == ALGO_PR) {   // only the owner holds a vertex's initial residual
+    if (g->multi && algo == ALGO_PR) {   // only the owner holds a vertex's initial residual
         if (c->v_lo) HYT_CUDA(cudaMemsetAsync(c->delta, 0, c->v_lo * 4, main));
         if (c->v_hi < g->V) HYT_CUDA(cudaMemsetAsync(c->delta + c->v_hi, 0, (g->V - c->v_hi) * 4, main));
     }
@@ -964,7 +972,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     g->launches = 1;
 
     // ---- fused peer push (exchange = 3): publish this rank's arrays, map the others' ----
-    const bool peer = g->world > 1 && P.exchange == 3;
+    const bool peer = g->multi && P.exchange == 3;
     PeerPush pp_it;
     const PeerPush *ppp = nullptr;
     struct PeerGuard {
@@ -1023,7 +1031,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         harvest(g, c);
         const SegHdr H = *c->hdr_h;
         uint64_t active = H.active_vertices, active_e = H.active_edges;
-        if (g->world > 1) {   // total active vertices (termination) and edges (direction switch) over all ranks
+        if (g->multi) {   // total active vertices (termination) and edges (direction switch) over all ranks
             HYT_CUDA(cudaMemcpyAsync(c->red, &c->hdr_d->active_vertices, 16, cudaMemcpyDeviceToDevice, main));
             dist_allreduce_sum_u64(g, c->red, 2, main);
             uint64_t a2[2] = {0, 0};
@@ -1155,7 +1163,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             timed_begin(c, main, e1, TAG_R);
             const uint32_t *nbr = reinterpret_cast<const uint32_t *>(c->cache) - c->cache_c0 * 4;
             const uint32_t *front = s.bm_cur;
-            if (g->world > 1) {   // OR of every rank's own frontier words (disjoint bits: a sum)
+            if (g->multi) {   // OR of every rank's own frontier words (disjoint bits: a sum)
                 launch_own_words(s.bm_cur, c->bm_glob, s.W, c->v_lo, c->v_hi, main);
                 HYT_CUDA(cudaMemsetAsync(c->bm_glob + s.W, 0, 8, main));
                 dist_allreduce_sum_u64(g, reinterpret_cast<uint64_t *>(c->bm_glob), (s.W + 1) / 2, main);
@@ -1245,7 +1253,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             HYT_CUDA(cudaMemsetAsync(c->red + 1, 0, 8, main));
             dist_allreduce_max_u64(g, c->red + 1, 1, main);
             g->stats.exch_peer += 1;
-        } else if (g->world > 1) {
+        } else if (g->multi) {
             const bool pr = algo == ALGO_PR;
             bool sparse = false;
             uint64_t maxc = 0;
@@ -1307,7 +1315,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         g->stats.edges_relaxed += row.active_edges;
         g->iter_log.push_back(row);
     }
-    if (g->world > 1 && algo == ALGO_PR) dist_allreduce_sum_f32(g, c->rank, g->V, main);
+    if (g->multi && algo == ALGO_PR) dist_allreduce_sum_f32(g, c->rank, g->V, main);
     if (peer && algo != ALGO_PR) dist_allreduce_min_u32(g, c->val, g->V, main);   // owners' values everywhere
     HYT_CUDA(cudaStreamSynchronize(main));
     harvest(g, c);
@@ -1398,7 +1406,7 @@ void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_par
     HYT_CUDA(cudaMemsetAsync(c->parts_d, 0, N * sizeof(PartIter), g->main));
     const PlanBufs pb{c->parts_d, c->iagg, c->ibase, c->hdr_d};
     launch_plan(s, c->bounds_d, c->t_d, c->items, 0, c->n_items, 0, N, c->cache_hi, g->prm.engine_mode,
-                cost_for(g, d1), pb, g->main);
+                cost_for(g, d1, algo), pb, g->main);
     std::vector<PartIter> ph(N);
     HYT_CUDA(cudaMemcpyAsync(ph.data(), c->parts_d, N * sizeof(PartIter), cudaMemcpyDeviceToHost, g->main));
     HYT_CUDA(cudaStreamSynchronize(g->main));

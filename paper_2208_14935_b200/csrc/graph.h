@@ -80,7 +80,7 @@ struct Params {
     double thpt_cpt_gbs = 0;   // host gather throughput (0 = measure)
     double link_gbs = 0;       // host->device link rate (0 = measure)
     double zc_weight = 1.0;    // multiplier on Tiz (1 = the paper's Eq. 3)
-    int cost_model = 1;        // 1: Eq. 1-3 with costs calibrated on this box; 0: the paper's PCIe-3 constants
+    int cost_model = 1;        // 1: Eq. 1-3 with costs calibrated on this box for BFS/SSSP/CC, the paper's for PR; 2: calibrated for all; 0: the paper's PCIe-3 constants
     double zc_req_ns = 0;      // zero-copy random 128-B request time (0 = measure)
     double zc_line_ns = 0;     // zero-copy streamed 128-B line time (0 = measure)
     uint64_t cal_probe_bytes = 4ull << 30;   // pinned probe buffer of the box calibration (>= 256 MiB)
@@ -170,6 +170,10 @@ struct hyt_graph {
     double est_zc_req_ns = 0, est_zc_line_ns = 0;          // zero-copy random request / stream line (cost_model = 1)
     // ---- multi-GPU ----
     int rank = 0, world = 1;
+    // joined a group (hyt_init_dist / hyt_init_dist_local): the run takes the
+    // multi-rank path (split, exchange, frontier merge) even at world 1, where every
+    // collective is an identity -- so the NCCL transport runs on a one-GPU box
+    bool multi = false;
     void *nccl_comm = nullptr;
     void *local_group = nullptr;   // in-process group (hyt_init_dist_local) instead of NCCL
     uint64_t local_key = 0;

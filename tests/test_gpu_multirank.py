@@ -254,3 +254,49 @@ def oracle_bfs_sym(gkey):
         g = symmetric_version(gkey)
         _bfs_sym_cache[gkey] = oracle.bfs(g.off, g.nbr, src_of(g))
     return _bfs_sym_cache[gkey]
+
+
+def run_nccl_world1(hyt, g, algo, engine="hybrid", part=4096, symmetric=False, **kw):
+    """One handle on a one-rank NCCL communicator (hyt_init_dist at world 1): the
+    run takes the multi-rank path -- split, per-iteration NCCL all-reduce / all-gather
+    or the CUDA-IPC peer push, owner frontier merge, global termination -- on the
+    transport a job uses, where each collective is an identity."""
+    import torch  # noqa: F401 -- loads torch's libnccl.so.2, which hyt dlopens
+    G = hyt.Graph(device=0)
+    try:
+        G.init_dist(0, 1, hyt.nccl_unique_id())
+        G.load(g.off, g.nbr, g.w, symmetric=symmetric)
+        G.set("engine_mode", engine)
+        G.set("partition_bytes", part)
+        for k, v in kw.items():
+            G.set(k, v)
+        G.run(algo, src_of(g) if algo in ("bfs", "sssp") else 0)
+        return G.values(), G.stats()
+    finally:
+        G.close()
+
+
+@pytest.mark.parametrize("exchange", [0, 2, 3])
+@pytest.mark.parametrize("engine", ["hybrid", "filter", "compaction", "zerocopy", "resident"])
+@pytest.mark.parametrize("algo", ["bfs", "sssp", "cc", "pr"])
+def test_nccl_world1(hyt, exchange, engine, algo):
+    """The NCCL transport itself (not the in-process group) on the one GPU a test box
+    has: dense all-reduce (0), sparse pair all-gather (2), CUDA-IPC peer push (3)."""
+    gkey = ("rmat", 9)
+    g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
+    vals, st = run_nccl_world1(hyt, g, algo, engine=engine, exchange=exchange)
+    check(gkey, algo, [(vals, st)])
+    if exchange == 3:
+        assert st["exch_peer"] == st["iterations"] > 0
+    else:
+        assert st["exch_sparse"] + st["exch_dense"] == st["iterations"] > 0
+        assert (st["exch_sparse"] > 0) == (exchange == 2)
+
+
+@pytest.mark.parametrize("direction", [1, 2])
+def test_nccl_world1_pull(hyt, direction):
+    """Pull BFS across the NCCL path (frontier words all-reduced every pull iteration)."""
+    gkey = ("rmat", 9)
+    g = symmetric_version(gkey)
+    vals, st = run_nccl_world1(hyt, g, "bfs", engine="resident", symmetric=True, direction=direction, exchange=0)
+    check(gkey, "bfs", [(vals, st)])

@@ -48,7 +48,7 @@ def main():
     for mode in a.modes.split(","):
         G.set("edge_cache", 1 if "+cache" in mode else 0)
         G.set("cpu_cost", 1 if "+cpu" in mode else 0)
-        G.set("cost_model", 1 if "+cal" in mode else 0)
+        G.set("cost_model", 2 if "+cal" in mode else 0)
         zw = [x for x in mode.split("+") if x.startswith("zw")]
         G.set("zc_weight", float(zw[0][2:]) if zw else 1.0)
         G.set("direction", 2 if "+pullall" in mode else 1 if "+pull" in mode else 0)
