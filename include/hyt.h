@@ -130,7 +130,6 @@ typedef struct {
     uint64_t exch_peer;            /* iterations exchanged by fused peer push (exchange = 3) */
     uint64_t host_store_bytes;     /* pinned host bytes the library owns for this rank's  */
                                    /* edge store (0 for adopted ids, HYT_ADOPT_HOST)      */
-    uint64_t units_deferred;       /* PR filter units deferred over the run (pr_defer)    */
 } hyt_stats;
 
 /* One row per iteration (hyt_get_iter_log), the Fig. 7 / Table VI analog. */
@@ -140,8 +139,6 @@ typedef struct {
     uint32_t parts_f, parts_c, parts_z, parts_r;
     uint32_t units_f;
     uint32_t dir;                  /* 0 push (data-driven), 1 pull (topology-driven) */
-    uint32_t units_deferred;       /* PR filter units left for later (pr_defer)    */
-    uint32_t pad_;
     uint64_t bytes_f, bytes_c, bytes_z;
     double   ms;                   /* wall time of the iteration                  */
 } hyt_iter;
@@ -219,10 +216,6 @@ int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off_ho
  *   recompute [1] (process a loaded filter unit once more);
  *   damping [0.85], epsilon [1e-5], max_iters [1000] (PR; the per-vertex
  *   relative truncation error is at most epsilon/(1-d) = 6.7e-5);
- *   pr_defer [0]: theta in [0, 1]; a PR filter unit whose delta mass per
- *   transferred byte is below theta x the iteration's best is left for a later
- *   iteration (its vertices stay active, so termination and the error bound
- *   are unchanged; the delta-driven priority of P:464-465 across iterations);
  *   gather_threads [0 = all cores]; compaction_buffer_bytes [0 = auto];
  *   edge_cache [0]: 1 keeps the longest hub-order prefix of partitions that fits
  *   the budget left after the run buffers resident in device memory (served as

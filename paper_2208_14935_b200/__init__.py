@@ -50,16 +50,14 @@ class hyt_stats(ctypes.Structure):
         ("cal_link_gbs", ctypes.c_double), ("cal_cpt_gbs", ctypes.c_double), ("cal_zc_req_ns", ctypes.c_double),
         ("cal_zc_line_ns", ctypes.c_double), ("exch_sparse", ctypes.c_uint64), ("exch_dense", ctypes.c_uint64),
         ("exch_bytes", ctypes.c_uint64), ("pull_iters", ctypes.c_uint64), ("um_balloon_bytes", ctypes.c_uint64),
-        ("exch_peer", ctypes.c_uint64), ("host_store_bytes", ctypes.c_uint64),
-        ("units_deferred", ctypes.c_uint64)]
+        ("exch_peer", ctypes.c_uint64), ("host_store_bytes", ctypes.c_uint64)]
 
 
 class hyt_iter(ctypes.Structure):
     _fields_ = [("iteration", ctypes.c_uint64), ("active_vertices", ctypes.c_uint64),
                 ("active_edges", ctypes.c_uint64), ("parts_f", ctypes.c_uint32), ("parts_c", ctypes.c_uint32),
                 ("parts_z", ctypes.c_uint32), ("parts_r", ctypes.c_uint32), ("units_f", ctypes.c_uint32),
-                ("dir", ctypes.c_uint32), ("units_deferred", ctypes.c_uint32), ("pad_", ctypes.c_uint32),
-                ("bytes_f", ctypes.c_uint64), ("bytes_c", ctypes.c_uint64),
+                ("dir", ctypes.c_uint32), ("bytes_f", ctypes.c_uint64), ("bytes_c", ctypes.c_uint64),
                 ("bytes_z", ctypes.c_uint64), ("ms", ctypes.c_double)]
 
 

@@ -1100,32 +1100,11 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             HYT_CUDA(cudaMemcpyAsync(c->cq_pre, c->q.qpre + H.ent_base[ENG_C], nC * 8, cudaMemcpyDeviceToHost, main));
         }
 
-        // ---- delta-PR deferral (pr_defer = theta > 0): a filter unit whose delta mass
-        // per transferred byte is below theta x the iteration's best is left for a later
-        // iteration, where it transfers the same bytes for more accumulated mass.
-        // Its vertices stay active (delta > eps), so termination is unchanged. ----
-        std::vector<uint8_t> defer((size_t)nu, 0);
-        if (algo == ALGO_PR && P.pr_defer > 0 && nu > 1) {
-            std::vector<double> dens((size_t)nu);
-            double best = 0;
-            for (int64_t j = 0; j < nu; ++j) {
-                const uint64_t pa = c->p_lo + units[2 * j], pb = c->p_lo + units[2 * j + 1];
-                double m = 0;
-                for (uint64_t i = pa; i < pb; ++i) m += c->parts_h[i].dsum;
-                const uint64_t by = (chunk_hi(g->off_h[c->bounds[pb]], c->d1) - chunk_lo(g->off_h[c->bounds[pa]], c->d1)) * 16;
-                dens[j] = m / (double)(by ? by : 1);
-                best = std::max(best, dens[j]);
-            }
-            for (int64_t j = 0; j < nu; ++j)
-                if (dens[j] < P.pr_defer * best) { defer[j] = 1; row.units_deferred += 1; }
-        }
         // ---- filter units, in priority order ----
         const uint64_t fseg_first = H.ent_base[ENG_F], fseg_end = fseg_first + H.ent_count[ENG_F];
-        int64_t ran = 0;
         for (int64_t jj = 0; jj < nu; ++jj) {
             const uint32_t j = order[jj];
-            if (defer[j]) continue;
-            const int si = (int)(ran++ % c->S);
+            const int si = (int)(jj % c->S);
             cudaStream_t stm = g->st[si];
             const uint64_t pa = c->p_lo + units[2 * j], pb = c->p_lo + units[2 * j + 1];
             const uint64_t v_lo = c->bounds[pa], v_hi = c->bounds[pb];
@@ -1333,7 +1312,6 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
         g->stats.parts_zerocopy += row.parts_z;
         g->stats.parts_resident += row.parts_r;
         g->stats.units_filter += row.units_f;
-        g->stats.units_deferred += row.units_deferred;
         g->stats.edges_relaxed += row.active_edges;
         g->iter_log.push_back(row);
     }

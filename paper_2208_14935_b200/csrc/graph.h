@@ -62,7 +62,6 @@ struct Params {
     int engine_mode = MODE_HYBRID;
     int priority = -1;
     int recompute = 1;
-    double pr_defer = 0.0;     // PR: defer filter units below this fraction of the best delta mass per byte (0 = off)
     double damping = 0.85, epsilon = 1e-5;   // C16 (round 2): eps/(1-d) = 6.7e-5 < 1e-4
     uint64_t max_iters = 1000;
     int gather_threads = 0;

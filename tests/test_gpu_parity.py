@@ -436,19 +436,3 @@ def test_destination_bands(hyt, bands, algo):
                 assert_pr_close(got, want)
             else:
                 assert np.array_equal(got, want)
-
-
-@pytest.mark.parametrize("theta", [0.05, 0.5, 1.0])
-@pytest.mark.parametrize("engine", ["hybrid", "filter"])
-@pytest.mark.parametrize("gi", [9, 13])
-def test_pr_defer(hyt, theta, engine, gi):
-    """pr_defer: filter units with little delta mass per byte wait for a later
-    iteration; the fixed point and its 1e-4 bar are unchanged (vertices stay active
-    until delta <= eps), and units are really deferred."""
-    gkey = ("rmat", gi)
-    g = gkey_graph(gkey)
-    got, st, log = run_gpu(hyt, g, "pr", engine=engine, part=4096, pr_defer=theta)
-    assert_pr_close(got, expected(gkey, "pr"))
-    assert st["units_deferred"] == sum(r["units_deferred"] for r in log)
-    if theta == 1.0:
-        assert st["units_deferred"] > 0

@@ -50,7 +50,7 @@ def main():
             row = {"ms": ms, "iterations": st["iterations"],
                    "xfer_over_edges": (st["bytes_filter"] + st["bytes_compaction"] + st["bytes_zerocopy"]) / (4 * g.E),
                    "parts_fcz": [st["parts_filter"], st["parts_compaction"], st["parts_zerocopy"]],
-                   "edges_relaxed": st["edges_relaxed"], "units_deferred": st["units_deferred"]}
+                   "edges_relaxed": st["edges_relaxed"]}
             if want is not None:
                 v = G.values().astype(np.float64)
                 row["max_rel_err"] = float(np.max(np.abs(v - want) / want))
@@ -66,7 +66,7 @@ def main():
         out["rows"][setting] = {"summary": summ, "runs": rows}
         print(setting, json.dumps(summ), flush=True)
         for k in kv:   # back to defaults
-            G.set(k, {"cost_model": 1, "epsilon": 1e-5, "zc_weight": 1.0, "relax_bands": 1, "pr_defer": 0}.get(k, 0))
+            G.set(k, {"cost_model": 1, "epsilon": 1e-5, "zc_weight": 1.0, "relax_bands": 1}.get(k, 0))
     G.close()
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:
