@@ -213,7 +213,8 @@ int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off_ho
  *   partition_bytes [33554432]; hub_fraction [0.08] (load time);
  *   streams [4]; engine_mode [HYT_MODE_HYBRID]; priority [-1 = auto:
  *   delta for PR, hub otherwise; 0 none, 1 hub, 2 delta];
- *   recompute [1] (process a loaded filter unit once more);
+ *   recompute [1] (process a loaded filter unit once more; 0-8 passes,
+ *   > 1 is Subway-style multi-round processing, measured slower on PR);
  *   damping [0.85], epsilon [1e-5], max_iters [1000] (PR; the per-vertex
  *   relative truncation error is at most epsilon/(1-d) = 6.7e-5);
  *   gather_threads [0 = all cores]; compaction_buffer_bytes [0 = auto];

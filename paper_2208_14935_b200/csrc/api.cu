@@ -125,7 +125,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "streams") { integral(); in(1, 8); p.streams = (int)v; }
         else if (k == "engine_mode") { integral(); in(0, 5); p.engine_mode = (int)v; }
         else if (k == "priority") { integral(); in(-1, 2); p.priority = (int)v; }
-        else if (k == "recompute") { integral(); in(0, 1); p.recompute = (int)v; }
+        else if (k == "recompute") { integral(); in(0, 8); p.recompute = (int)v; }
         else if (k == "damping") { in(1e-6, 1 - 1e-6); p.damping = v; }
         else if (k == "epsilon") { in(0, 1); p.epsilon = v; }
         else if (k == "max_iters") { integral(); in(1, 1e9); p.max_iters = (uint64_t)v; }

@@ -1127,7 +1127,9 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
             launch_relax(s, c->q, H.tile_base[ENG_F], fseg_first, fseg_end, H.chunk_total[ENG_F], c_lo, c_hi,
                          nullptr, es, relax_ctas, stm, P.relax_hot, ppp);
             timed_end(c, stm, e2);
-            if (P.recompute) {   // process the loaded unit exactly once more
+            // process the loaded unit once more; recompute > 1 repeats
+            // the pass (Subway-style multi-round processing of the staged unit)
+            for (int rp = 0; rp < P.recompute; ++rp) {
                 EvPair e4;
                 timed_begin(c, stm, e4, TAG_RQ);
                 launch_range_queue(s, v_lo, v_hi, c->rb[si], stm);
@@ -1136,7 +1138,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
                 launch_relax(s, c->rb[si].q, 0, 0, 0, 0, 0, 0, c->rb[si].total, es, relax_ctas, stm, P.relax_hot, ppp);
                 timed_end(c, stm, e3);
             }
-            g->launches += P.recompute ? 4 : 1;
+            g->launches += 1 + 3 * P.recompute;
             row.bytes_f += bytes;
             g->eng_chunks[ENG_F] += c_hi - c_lo;
             for (uint64_t i = pa; i < pb; ++i) g->eng_edges[ENG_F] += c->parts_h[i].e;
