@@ -24,7 +24,7 @@ hytgen/libhytgen.so: hytgen/hytgen.c
 oracle/liboracle.so: oracle/oracle.c
 	gcc -O3 -march=x86-64-v3 -ffp-contract=off -fPIC -shared -pthread -o $@ $< -lm
 
-tools: tools/pin_bench tools/zc_bench tools/scatter_bench
+tools: tools/pin_bench tools/zc_bench tools/scatter_bench tools/red_ceiling
 
 tools/pin_bench: tools/pin_bench.cu
 	$(NVCC) $(ARCH) -O2 -o $@ $< -lpthread
@@ -35,7 +35,10 @@ tools/zc_bench: tools/zc_bench.cu
 tools/scatter_bench: tools/scatter_bench.cu
 	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
 
+tools/red_ceiling: tools/red_ceiling.cu
+	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
+
 clean:
-	rm -rf build $(LIB) hytgen/libhytgen.so oracle/liboracle.so tools/pin_bench tools/zc_bench tools/scatter_bench
+	rm -rf build $(LIB) hytgen/libhytgen.so oracle/liboracle.so tools/pin_bench tools/zc_bench tools/scatter_bench tools/red_ceiling
 
 .PHONY: all clean tools

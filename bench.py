@@ -650,6 +650,17 @@ def main():
         except (OSError, ValueError):
             pattern = None
 
+    # the L2 reduction ceiling swept over launch shapes and PTX forms (tools/red_ceiling.cu):
+    # the best rate any configuration reached into an L2-resident array
+    red_ceiling, red_src = None, None
+    rf = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_red_ceiling.json")))
+    if rf:
+        try:
+            red_ceiling = max(r["g_per_s"] for r in json.load(open(rf[-1]))["rows"])
+            red_src = "profiles/" + os.path.basename(rf[-1])
+        except (OSError, ValueError, KeyError):
+            red_ceiling = None
+
     def tag_roof(i):
         if eng_launch[i] == 0:
             return None
@@ -671,10 +682,13 @@ def main():
             # one random 4-B destination access per edge into an L2-resident array
             # (tools/scatter_bench.cu; red.add.f32 for PR, a load for the min-algorithms)
             ceil_red = pattern["uniform_l2_resident"]["red_add"]["gedges_s"]
+            if red_ceiling:
+                ceil_red = max(ceil_red, red_ceiling)
             ceil_ld = pattern["uniform_l2_resident"]["ld"]["gedges_s"]
             eps = eng_edges[i] / eng_launch[i] / avg_s / 1e9
             r["access_pattern"] = {"achieved_gedges_s": eps, "ceiling_red_add_gedges_s": ceil_red,
-                                   "ceiling_load_gedges_s": ceil_ld, "source": pattern_src,
+                                   "ceiling_load_gedges_s": ceil_ld,
+                                   "source": pattern_src + (f" + {red_src}" if red_src else ""),
                                    "note": "random 4-B destination accesses per second; the HBM-copy frac above "
                                            "counts them as 4 B each"}
         r["traffic"] = None
