@@ -24,7 +24,7 @@ hytgen/libhytgen.so: hytgen/hytgen.c
 oracle/liboracle.so: oracle/oracle.c
 	gcc -O3 -march=x86-64-v3 -ffp-contract=off -fPIC -shared -pthread -o $@ $< -lm
 
-tools: tools/pin_bench tools/zc_bench tools/scatter_bench tools/red_ceiling
+tools: tools/pin_bench tools/zc_bench tools/scatter_bench tools/red_ceiling tools/dsmem_bench
 
 tools/pin_bench: tools/pin_bench.cu
 	$(NVCC) $(ARCH) -O2 -o $@ $< -lpthread
@@ -38,7 +38,10 @@ tools/scatter_bench: tools/scatter_bench.cu
 tools/red_ceiling: tools/red_ceiling.cu
 	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
 
+tools/dsmem_bench: tools/dsmem_bench.cu
+	$(NVCC) $(ARCH) -O3 -std=c++17 -o $@ $<
+
 clean:
-	rm -rf build $(LIB) hytgen/libhytgen.so oracle/liboracle.so tools/pin_bench tools/zc_bench tools/scatter_bench tools/red_ceiling
+	rm -rf build $(LIB) hytgen/libhytgen.so oracle/liboracle.so tools/pin_bench tools/zc_bench tools/scatter_bench tools/red_ceiling tools/dsmem_bench
 
 .PHONY: all clean tools
