@@ -686,7 +686,8 @@ def main():
                 ceil_red = max(ceil_red, red_ceiling)
             ceil_ld = pattern["uniform_l2_resident"]["ld"]["gedges_s"]
             eps = eng_edges[i] / eng_launch[i] / avg_s / 1e9
-            r["access_pattern"] = {"achieved_gedges_s": eps, "ceiling_red_add_gedges_s": ceil_red,
+            r["access_pattern"] = {"achieved_gedges_s": eps, "ceiling_red_add_gedges_s": ceil_red,  # hub-block edges included
+                                   "frac_of_red_add_ceiling": eps / ceil_red,
                                    "ceiling_load_gedges_s": ceil_ld,
                                    "source": pattern_src + (f" + {red_src}" if red_src else ""),
                                    "note": "random 4-B destination accesses per second; the HBM-copy frac above "
