@@ -661,6 +661,10 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
 
 // One cached context per algorithm; when the budget cannot hold another one,
 // the others are dropped and the build is retried.
+static inline double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 static RunCtx *get_ctx(hyt_graph *g, int algo) {
     RunCtx *&c = ctx_of(g, algo);
     if (c) return c;
@@ -672,7 +676,9 @@ static RunCtx *get_ctx(hyt_graph *g, int algo) {
         if (g->last_algo != algo) g->has_result = false;
     }
     try {
+        const double t0 = now_ms();
         c = build_ctx(g, algo);
+        if (getenv("HYT_VERBOSE")) fprintf(stderr, "[hyt run] context for algo %d built in %.1f ms\n", algo, now_ms() - t0);
     } catch (const Err &e) {
         if (e.code != HYT_ENOMEM) throw;
         for (int a = 0; a < 4; ++a)
@@ -727,7 +733,6 @@ void gather_window(RunCtx *c, const uint4 *edges_host, const std::vector<uint64_
     });
 }
 
-static inline double now_ms();
 
 // ---------------------------------------------------------------------------
 // Cost-model calibration on this box.  Box properties (the DMA
@@ -880,9 +885,6 @@ static CostParams cost_for(hyt_graph *g, uint32_t d1, int algo) {
     return make_cost(P, d1, ratio, zr, zs);
 }
 
-static inline double now_ms() {
-    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
 
 void run_graph(hyt_graph *g, int algo, uint64_t source) {
     HYT_REQUIRE(g->loaded, HYT_ESTATE, "no graph loaded");

@@ -43,8 +43,17 @@ static uint64_t pin_cache_cap() {
     return cap;
 }
 
+static bool pin_verbose() {
+    static const bool v = getenv("HYT_VERBOSE") != nullptr;
+    return v;
+}
+static double pin_now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void *pinned_alloc(uint64_t bytes) {
     const uint64_t huge = 2ull << 20;
+    const double t0 = pin_now_ms();
     const uint64_t len = (bytes + huge - 1) / huge * huge;
     {   // a cached block of at least len and at most 5/4 of it (contents are not zeroed:
         // every user writes what it reads; the edge store's padding is never interpreted)
@@ -83,14 +92,20 @@ void *pinned_alloc(uint64_t bytes) {
         munmap(p, len);
         throw Err{HYT_ENOMEM, std::string("cudaHostRegister failed: ") + cudaGetErrorString(e)};
     }
+    if (pin_verbose() && len >= (64ull << 20))
+        fprintf(stderr, "[hyt pin] new block %8.3f GB  %7.1f ms (cache holds %.3f GB)\n", len / 1e9,
+                pin_now_ms() - t0, g_pin_cached / 1e9);
     std::lock_guard<std::mutex> l(g_pin_mu);
     g_pinned[p] = len;
     return p;
 }
 
 static void pin_release(void *p, uint64_t len) {
+    const double t0 = pin_now_ms();
     cudaHostUnregister(p);
     munmap(p, len);
+    if (pin_verbose() && len >= (64ull << 20))
+        fprintf(stderr, "[hyt pin] released %8.3f GB  %7.1f ms\n", len / 1e9, pin_now_ms() - t0);
 }
 
 void pinned_free(void *p) {
@@ -147,7 +162,17 @@ __global__ void k_indeg(const uint32_t *__restrict__ nbr, uint64_t E, uint64_t V
     };
     if (tid < head) one(nbr[tid]);
     const uint4 *v4 = reinterpret_cast<const uint4 *>(nbr + head);
-    for (uint64_t i = tid; i < nvec; i += stride) {
+    // 4 coalesced 16-byte loads in flight per thread before the atomics (the ids
+    // are read over the host link)
+    uint64_t i = tid;
+    for (; i + 3 * stride < nvec; i += 4 * stride) {
+        uint4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = v4[i + u * stride];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { one(q[u].x); one(q[u].y); one(q[u].z); one(q[u].w); }
+    }
+    for (; i < nvec; i += stride) {
         const uint4 q = v4[i];
         one(q.x); one(q.y); one(q.z); one(q.w);
     }
@@ -307,18 +332,40 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
             }
             __syncthreads();
             const uint64_t stop = min(e_end, s_new[nr]);   // edges the staged rows cover
-            for (uint64_t x = e + threadIdx.x; x < stop; x += blockDim.x) {
-                int lo = 0, hi = (int)nr - 1;              // last staged row starting <= x
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (s_new[mid] <= x) lo = mid; else hi = mid - 1;
+            // kU coalesced slots per thread per round, all loads issued before any use:
+            // the caller's arrays are read over the host link, where one 4-byte load in
+            // flight per thread leaves the link idle
+            constexpr int kU = 4;
+            for (uint64_t x0 = e + threadIdx.x; x0 < stop; x0 += (uint64_t)kU * blockDim.x) {
+                uint64_t src[kU];
+                uint32_t id[kU], wt[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const uint64_t x = x0 + (uint64_t)u * blockDim.x;
+                    src[u] = ~0ull;
+                    if (x < stop) {
+                        int lo = 0, hi = (int)nr - 1;      // last staged row starting <= x
+                        while (lo < hi) {
+                            const int mid = (lo + hi + 1) >> 1;
+                            if (s_new[mid] <= x) lo = mid; else hi = mid - 1;
+                        }
+                        src[u] = s_old[lo] + (x - s_new[lo]);
+                    }
                 }
-                const uint64_t src = s_old[lo] + (x - s_new[lo]);
-                const uint32_t id = nbr_in[src];
-                if (id >= V) { *bad = 1; continue; }
-                const uint32_t y = new_id[id];
-                if (nbr_out) nbr_out[x] = y;
-                if (ew_out) ew_out[x] = (uint64_t)y | ((uint64_t)w_in[src] << 32);
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    id[u] = src[u] != ~0ull ? nbr_in[src[u]] : 0u;
+                    wt[u] = (ew_out && src[u] != ~0ull) ? w_in[src[u]] : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    if (src[u] == ~0ull) continue;
+                    const uint64_t x = x0 + (uint64_t)u * blockDim.x;
+                    if (id[u] >= V) { *bad = 1; continue; }
+                    const uint32_t y = new_id[id[u]];
+                    if (nbr_out) nbr_out[x] = y;
+                    if (ew_out) ew_out[x] = (uint64_t)y | ((uint64_t)wt[u] << 32);
+                }
             }
             e = stop;
         }
