@@ -450,9 +450,21 @@ static void ensure_cq(RunCtx *c, uint64_t n) {
     c->cq_cap = cap;
 }
 
+static inline double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 static RunCtx *build_ctx(hyt_graph *g, int algo) {
     const Params &P = g->prm;
     RunCtx *c = new RunCtx();
+    const bool verbose = getenv("HYT_VERBOSE") != nullptr;
+    double tm = now_ms();
+    auto mark = [&](const char *what) {
+        if (!verbose) return;
+        const double t = now_ms();
+        fprintf(stderr, "[hyt ctx]   %-34s %8.1f ms\n", what, t - tm);
+        tm = t;
+    };
     try {
         c->algo = algo;
         c->d1 = (algo == ALGO_SSSP) ? 8 : 4;
@@ -483,6 +495,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         } else {
             c->val = dalloc<uint32_t>(g, c, V, "values");
         }
+        mark("bounds + vertex state");
         c->bm_a = dalloc<uint32_t>(g, c, W + 1, "frontier");
         c->bm_b = dalloc<uint32_t>(g, c, W + 1, "next frontier");
         c->bounds_d = dalloc<uint64_t>(g, c, c->N + 1, "partition bounds");
@@ -518,6 +531,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
             c->iagg = dalloc<ItemAgg>(g, c, c->n_items, "item aggregates");
             c->ibase = dalloc<uint64_t>(g, c, 2 * c->n_items, "item bases");
         }
+        mark("plan items");
         // queue: at most one entry per vertex with out-edges
         uint64_t vnz = 0, max_part_v = 0;
         for (uint64_t v = 0; v < V; ++v) vnz += g->off_h[v + 1] > g->off_h[v];
@@ -530,6 +544,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
         c->q.qdeg = dalloc<uint32_t>(g, c, c->q.cap, "queue degree");
         c->q.qaux = algo == ALGO_PR ? dalloc<float>(g, c, c->q.cap, "queue contrib") : nullptr;
         c->q.tile = dalloc<uint32_t>(g, c, c->q.tile_cap, "tile map");
+        mark("queue");
         // ---- host copies of the plan ----
         c->parts_h = halloc<PartIter>(c, c->N);
         c->hdr_h = halloc<SegHdr>(c, 1);
@@ -596,6 +611,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
                 r.acc = c->racc;
                 c->rb.push_back(r);
             }
+            mark("staging slots + range queues");
             // compaction double buffer: what is left (capped), at least cmin
             uint64_t cb = P.compaction_buffer_bytes;
             if (!cb) {
@@ -620,6 +636,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
             unsigned nt = P.gather_threads > 0 ? (unsigned)P.gather_threads
                                                : std::max(1u, std::thread::hardware_concurrency());
             c->pool = new Pool(nt);
+            mark("compaction buffers + gather pool");
             if (P.edge_cache && P.engine_mode == MODE_HYBRID) {
                 // partial resident edge cache: the longest prefix of the
                 // own partitions in hub order that fits what the budget has left
@@ -661,9 +678,6 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
 
 // One cached context per algorithm; when the budget cannot hold another one,
 // the others are dropped and the build is retried.
-static inline double now_ms() {
-    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
 
 static RunCtx *get_ctx(hyt_graph *g, int algo) {
     RunCtx *&c = ctx_of(g, algo);
