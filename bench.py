@@ -50,8 +50,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "GTEPS and time-to-converge per algo at 1/2/4/8 B200, % HBM/PCIe peak"
-L2_NOTE = ("inputs larger than L2: edges live in pinned host memory (11.8 GB packed id+weight, "
-           "5.9 GB ids) and the vertex state (0.5 GB) exceeds the 126 MB L2")
+L2_NOTE = ("inputs larger than L2: edges live in pinned host memory (5.9 GB of SSSP records packed as "
+           "id | w << 26, 5.9 GB ids) and the vertex state (0.5 GB) exceeds the 126 MB L2")
 
 
 def parse():

@@ -130,6 +130,8 @@ typedef struct {
     uint64_t exch_peer;            /* iterations exchanged by fused peer push (exchange = 3) */
     uint64_t host_store_bytes;     /* pinned host bytes the library owns for this rank's  */
                                    /* edge store (0 for adopted ids, HYT_ADOPT_HOST)      */
+    uint64_t record_bytes;         /* bytes per edge record the run read: 4 (ids, or SSSP  */
+                                   /* records packed as id | w << bits(V-1)) or 8 (id, w) */
 } hyt_stats;
 
 /* One row per iteration (hyt_get_iter_log), the Fig. 7 / Table VI analog. */
@@ -213,6 +215,9 @@ int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off_ho
  *   partition_bytes [33554432]; hub_fraction [0.08] (load time);
  *   streams [4]; engine_mode [HYT_MODE_HYBRID]; priority [-1 = auto:
  *   delta for PR, hub otherwise; 0 none, 1 hub, 2 delta];
+ *   pack_weights [1] (load time, set before hyt_load_csr): store SSSP records as
+ *   one u32, id | w << bits(V-1), when every weight fits the remaining bits (else
+ *   the (id, w) u64 records); halves SSSP's host-link bytes;
  *   recompute [1] (process a loaded filter unit once more; 0-8 passes,
  *   > 1 is Subway-style multi-round processing, measured slower on PR);
  *   damping [0.85], epsilon [1e-5], max_iters [1000] (PR; the per-vertex

@@ -50,7 +50,8 @@ class hyt_stats(ctypes.Structure):
         ("cal_link_gbs", ctypes.c_double), ("cal_cpt_gbs", ctypes.c_double), ("cal_zc_req_ns", ctypes.c_double),
         ("cal_zc_line_ns", ctypes.c_double), ("exch_sparse", ctypes.c_uint64), ("exch_dense", ctypes.c_uint64),
         ("exch_bytes", ctypes.c_uint64), ("pull_iters", ctypes.c_uint64), ("um_balloon_bytes", ctypes.c_uint64),
-        ("exch_peer", ctypes.c_uint64), ("host_store_bytes", ctypes.c_uint64)]
+        ("exch_peer", ctypes.c_uint64), ("host_store_bytes", ctypes.c_uint64),
+        ("record_bytes", ctypes.c_uint64)]
 
 
 class hyt_iter(ctypes.Structure):

@@ -128,6 +128,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "recompute") { integral(); in(0, 8); p.recompute = (int)v; }
         else if (k == "damping") { in(1e-6, 1 - 1e-6); p.damping = v; }
         else if (k == "epsilon") { in(0, 1); p.epsilon = v; }
+        else if (k == "pack_weights") { integral(); in(0, 1); p.pack_weights = (int)v; }
         else if (k == "max_iters") { integral(); in(1, 1e9); p.max_iters = (uint64_t)v; }
         else if (k == "gather_threads") { integral(); in(0, 256); p.gather_threads = (int)v; }
         else if (k == "compaction_buffer_bytes") { integral(); in(0, 1e12); p.compaction_buffer_bytes = (uint64_t)v; }

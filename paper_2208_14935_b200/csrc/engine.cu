@@ -181,10 +181,18 @@ void rank_partitions(const std::vector<uint64_t> &off, const std::vector<uint64_
     *p_hi = std::lower_bound(bounds.begin(), bounds.end(), hi) - bounds.begin();
 }
 
-const uint4 *host_edges(const hyt_graph *g, uint32_t d1) {
-    const int i = d1 == 8 ? 1 : 0;
-    const uintptr_t base = (uintptr_t)(i ? (const void *)g->ew_h : (const void *)g->nbr_h);
-    return (const uint4 *)(base - g->store_c0[i] * 16);
+// The store an algorithm's relaxations read: SSSP the packed u32 records (pw_h) or
+// the u64 records (ew_h), the others the u32 ids; *c0 = the store's first chunk.
+const void *edge_store(const hyt_graph *g, int algo, uint64_t *c0) {
+    if (algo == ALGO_SSSP && !g->pw_h) { *c0 = g->store_c0[1]; return g->ew_h; }
+    *c0 = g->store_c0[0];
+    return algo == ALGO_SSSP ? (const void *)g->pw_h : (const void *)g->nbr_h;
+}
+
+const uint4 *host_edges(const hyt_graph *g, int algo) {
+    uint64_t c0 = 0;
+    const uintptr_t base = (uintptr_t)edge_store(g, algo, &c0);
+    return (const uint4 *)(base - c0 * 16);
 }
 
 // ---------------------------------------------------------------------------
@@ -376,7 +384,7 @@ static void fill_cache(hyt_graph *g, RunCtx *c, uint64_t p_hi_cache) {
     const uint64_t c0 = chunk_lo(g->off_h[c->bounds[c->p_lo]], c->d1);
     const uint64_t c1 = chunk_hi(g->off_h[c->bounds[p_hi_cache]], c->d1);
     c->cache = dalloc<uint4>(g, c, c1 - c0 + 1, "resident edge cache");
-    HYT_CUDA(copy_sync(c->cache, host_edges(g, c->d1) + c0, (c1 - c0) * 16, g->main));
+    HYT_CUDA(copy_sync(c->cache, host_edges(g, c->algo) + c0, (c1 - c0) * 16, g->main));
     c->cache_c0 = c0;
     c->cache_hi = p_hi_cache;
     c->cache_bytes = (c1 - c0) * 16;
@@ -391,7 +399,7 @@ static void fill_um(hyt_graph *g, RunCtx *c) {
     const uint64_t c1 = chunk_hi(g->off_h[c->bounds[c->p_hi]], c->d1);
     const uint64_t bytes = (c1 - c0 + 1) * 16;
     HYT_CUDA(cudaMallocManaged((void **)&c->um, bytes, cudaMemAttachGlobal));
-    const char *src = reinterpret_cast<const char *>(host_edges(g, c->d1) + c0);
+    const char *src = reinterpret_cast<const char *>(host_edges(g, c->algo) + c0);
     char *dst = reinterpret_cast<char *>(c->um);
     const uint64_t n = (c1 - c0) * 16;
     const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
@@ -467,7 +475,7 @@ static RunCtx *build_ctx(hyt_graph *g, int algo) {
     };
     try {
         c->algo = algo;
-        c->d1 = (algo == ALGO_SSSP) ? 8 : 4;
+        c->d1 = (algo == ALGO_SSSP && !g->pw_h) ? 8 : 4;   // packed SSSP records: 4 B per edge
         const uint64_t V = g->V, W = (V + 31) / 32;
         c->bounds = partition_bounds_ranked(g->off_h, c->d1, P.partition_bytes, g->world);
         c->N = c->bounds.size() - 1;
@@ -716,6 +724,7 @@ static DevState make_state(hyt_graph *g, RunCtx *c) {
     s.val = c->val; s.rank = c->rank; s.delta = c->delta;
     s.bm_cur = c->bm_a; s.bm_next = c->bm_b;
     s.d1 = c->d1; s.algo = c->algo;
+    s.wshift = (c->algo == ALGO_SSSP && c->d1 == 4) ? g->wshift : 0;
     s.damping = (float)g->prm.damping;
     s.epsilon = (float)g->prm.epsilon;
     s.hot_v = (uint32_t)g->prm.relax_hot_v;
@@ -848,7 +857,7 @@ static void calibrate(hyt_graph *g, RunCtx *c) {
         }
     }
     if (P.thpt_cpt_gbs > 0) g->est_cpt_gbs = P.thpt_cpt_gbs;
-    const uint4 *edges_host = host_edges(g, c->d1);
+    const uint4 *edges_host = host_edges(g, c->algo);
     if (g->est_cpt_gbs <= 0 && c->pool && c->cq_cap > 1 && c->v_hi > c->v_lo) {
         // the lists of up to 64K random own vertices with out-edges, gathered like the C engine
         std::vector<uint32_t> vs;
@@ -917,11 +926,11 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     const int prio = P.priority >= 0 ? P.priority : (algo == ALGO_PR ? 2 : 1);
     const int sms = num_sms();
     const int relax_ctas = sms * P.relax_ctas_per_sm, zc_ctas = sms * P.zc_ctas_per_sm;
-    const uint4 *edges_host = host_edges(g, c->d1);          // indexed by global chunk
-    const uint64_t store_c0 = g->store_c0[c->d1 == 8 ? 1 : 0];
+    const uint4 *edges_host = host_edges(g, c->algo);          // indexed by global chunk
+    uint64_t store_c0 = 0;
+    const void *store = edge_store(g, algo, &store_c0);
     const uint4 *edges_mapped = nullptr;                       // device view of the store's first chunk
-    HYT_CUDA(cudaHostGetDevicePointer((void **)&edges_mapped,
-                                      (void *)(c->d1 == 8 ? (const void *)g->ew_h : (const void *)g->nbr_h), 0));
+    HYT_CUDA(cudaHostGetDevicePointer((void **)&edges_mapped, const_cast<void *>(store), 0));
 
     // reset statistics
     g->stats = hyt_stats{};
@@ -1353,6 +1362,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     g->stats.cal_zc_req_ns = g->est_zc_req_ns;
     g->stats.cal_zc_line_ns = g->est_zc_line_ns;
     g->stats.host_store_bytes = g->store_bytes;
+    g->stats.record_bytes = c->d1;
     for (int i = 0; i < 8; ++i) { g->stats.eng_ms[i] = 0; g->stats.eng_launches[i] = 0; g->stats.eng_chunks[i] = 0; g->stats.eng_edges[i] = 0; }
     g->stats.eng_ms[0] = g->plan_time.ms; g->stats.eng_launches[0] = g->plan_time.launches;
     for (int i = 1; i < ENG_COUNT; ++i) {
@@ -1406,7 +1416,7 @@ void debug_plan(hyt_graph *g, int algo, const uint8_t *active, uint64_t *num_par
     HYT_REQUIRE(g->loaded, HYT_ESTATE, "no graph loaded");
     HYT_REQUIRE(algo >= ALGO_BFS && algo <= ALGO_PR, HYT_EINVAL, "unknown algorithm");
     HYT_CUDA(cudaSetDevice(g->device));
-    const uint32_t d1 = algo == ALGO_SSSP ? 8 : 4;
+    const uint32_t d1 = (algo == ALGO_SSSP && !g->pw_h) ? 8 : 4;   // as build_ctx
     std::vector<uint64_t> b = partition_bounds_ranked(g->off_h, d1, g->prm.partition_bytes, g->world);
     const uint64_t N = b.size() - 1;
     *num_parts = N;
@@ -1450,6 +1460,7 @@ void free_graph(hyt_graph *g) {
     release_adopted(g);
     pinned_free(g->nbr_h);
     pinned_free(g->ew_h);
+    pinned_free(g->pw_h);
     dist_free(g);
     g->arena.release_all();
 }

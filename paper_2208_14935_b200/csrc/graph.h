@@ -74,6 +74,7 @@ struct Params {
     uint64_t relax_hot_v = 16384;   // PR hub-block vertices in shared memory (8 B each: 128 KB; min-algorithms cap at kHotV)
     int relax_bands = 1;            // destination bands for device-resident edges: 1 off (default: measured slower), 0 auto (V*4 / (3/4 L2)), n
     int relax_threads = 0;          // relax CTA size: 0 auto (PR 1024: 1 CTA/SM sharing the hub block; else 512), 512, 1024
+    int pack_weights = 1;      // load time: SSSP records as one u32 (id | w << bits(V-1)) when the weights fit
     int edge_cache = 0;        // 1: keep a prefix of partitions resident; 0: paper semantics
     uint64_t edge_cache_bytes = 0;   // cap on the cache (0 = whatever the budget leaves)
     int cpu_cost = 0;          // 1: include Eq. 2's CPU term with Thpt_cpt calibrated on this box
@@ -133,7 +134,11 @@ struct hyt_graph {
     // 16-byte chunk store_c0[0] (u32 ids) / store_c0[1] (id | w<<32) of the global
     // edge byte space.  host_edges() returns pointers indexed by GLOBAL chunk.
     uint32_t *nbr_h = nullptr;      // pinned mapped u32 ids (+pad)
-    uint64_t *ew_h = nullptr;       // pinned mapped (id | w<<32) u64 (+pad), weighted only
+    uint64_t *ew_h = nullptr;       // pinned mapped (id | w<<32) u64 (+pad), weighted, unpacked only
+    // packed SSSP records (pack_weights): one u32 per edge, id | w << wshift, with
+    // wshift = the bits of V-1; used when every weight fits the remaining bits
+    uint32_t *pw_h = nullptr;
+    uint32_t wshift = 0;
     uint64_t store_v_lo = 0, store_v_hi = 0;
     uint64_t store_c0[2] = {0, 0};
     std::vector<uint64_t> off_h;    // host copy of offsets u64[V+1]
@@ -206,7 +211,8 @@ void rank_partitions(const std::vector<uint64_t> &off, const std::vector<uint64_
                      uint64_t *p_lo, uint64_t *p_hi);
 // host pointer to the edge store of record width d1, indexed by GLOBAL 16-byte
 // chunk (valid for the chunks of the store's vertex range only)
-const uint4 *host_edges(const hyt_graph *g, uint32_t d1);
+const void *edge_store(const hyt_graph *g, int algo, uint64_t *c0);
+const uint4 *host_edges(const hyt_graph *g, int algo);
 // multi-GPU exchange (dist.cu)
 void dist_init(hyt_graph *g, int rank, int world, const void *uid);
 void dist_init_local(hyt_graph *g, int rank, int world, uint64_t group);

@@ -42,6 +42,8 @@ inline int num_sms() {
 }
 
 enum Algo : int { ALGO_BFS = 0, ALGO_SSSP = 1, ALGO_CC = 2, ALGO_PR = 3 };
+// k_relax instantiation of SSSP over packed 4-byte records (id | w << wshift)
+constexpr int ALGO_SSSP_PACKED = 4;
 enum Eng : int { ENG_NONE = 0, ENG_F = 1, ENG_C = 2, ENG_Z = 3, ENG_R = 4, ENG_COUNT = 5 };
 enum Mode : int { MODE_HYBRID = 0, MODE_FILTER = 1, MODE_COMPACTION = 2, MODE_ZEROCOPY = 3, MODE_RESIDENT = 4, MODE_UM = 5 };
 
@@ -123,6 +125,7 @@ struct DevState {
     float *rank, *delta;        // f32[V] PR
     uint32_t *bm_cur, *bm_next; // u32[W]
     uint32_t d1;
+    uint32_t wshift;            // SSSP with d1 = 4: packed records, weight = record >> wshift
     int algo;
     float damping, epsilon;
     uint32_t hot_v;             // hub-block size in shared memory (relax_hot_v)

@@ -147,7 +147,7 @@ __device__ __forceinline__ void hub_add_fx(uint32_t *lo, uint32_t *hi, uint32_t 
 template <int ALGO, bool COMPACT, bool PEER, int NT>
 __global__ void __launch_bounds__(NT, NT >= 1024 ? 1 : 2)
 k_relax(RelaxArgs A) {
-    constexpr uint32_t D1 = (ALGO == ALGO_SSSP) ? 8u : 4u;
+    constexpr uint32_t D1 = (ALGO == ALGO_SSSP) ? 8u : 4u;   // ALGO_SSSP_PACKED: 4-byte records
     constexpr int EPC = 16 / D1;                  // edge records per chunk
     constexpr bool PR = (ALGO == ALGO_PR);
     constexpr int kWarps = NT / 32;
@@ -299,13 +299,16 @@ k_relax(RelaxArgs A) {
                         for (int qd = 0; qd < EPC; ++qd) {
                             uint32_t d, wgt = 0;
                             if (D1 == 8) { d = words[2 * qd]; wgt = words[2 * qd + 1]; }
-                            else d = words[qd];
+                            else if (ALGO == ALGO_SSSP_PACKED) {
+                                d = words[qd] & ((1u << S.wshift) - 1u);
+                                wgt = words[qd] >> S.wshift;
+                            } else d = words[qd];
                             // this band's destinations only (hubs: band 0)
                             const bool ok = qd >= lo && qd < hi &&
                                             (d < n_hot ? band == 0 : (d >= b_lo && d < b_hi));
                             uint32_t cnd;
                             if (ALGO == ALGO_BFS) cnd = src + 1u;
-                            else if (ALGO == ALGO_SSSP) {
+                            else if (ALGO == ALGO_SSSP || ALGO == ALGO_SSSP_PACKED) {
                                 const uint64_t c64 = (uint64_t)src + wgt;
                                 cnd = c64 >= kInf ? kInf - 1u : (uint32_t)c64;
                             } else cnd = src;
@@ -464,7 +467,10 @@ void launch_relax(const DevState &s, const QueueBufs &q, uint64_t tile_base, uin
     else { HYT_RELAX_B(ALG, false) }
     switch (s.algo) {
         case ALGO_BFS: HYT_RELAX(ALGO_BFS); break;
-        case ALGO_SSSP: HYT_RELAX(ALGO_SSSP); break;
+        case ALGO_SSSP:
+            if (s.d1 == 4) { HYT_RELAX(ALGO_SSSP_PACKED); }
+            else { HYT_RELAX(ALGO_SSSP); }
+            break;
         case ALGO_CC: HYT_RELAX(ALGO_CC); break;
         default: HYT_RELAX(ALGO_PR); break;
     }

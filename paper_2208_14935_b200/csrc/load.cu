@@ -299,7 +299,9 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
                 const uint32_t *__restrict__ old_of, const uint32_t *__restrict__ new_id,
                 const uint64_t *__restrict__ row_start, uint64_t r_base, uint64_t r_end,
                 const uint32_t *__restrict__ nbr_in, const uint32_t *__restrict__ w_in,
-                uint32_t *__restrict__ nbr_out, uint64_t *__restrict__ ew_out, uint32_t *__restrict__ bad) {
+                uint32_t *__restrict__ nbr_out, uint64_t *__restrict__ ew_out,
+                uint32_t *__restrict__ pw_out, uint32_t wshift, uint32_t *__restrict__ wbig,
+                uint32_t *__restrict__ bad) {
     __shared__ uint64_t s_new[kRelabelRows + 1];
     __shared__ uint64_t s_old[kRelabelRows];
     __shared__ uint64_t s_r0;
@@ -355,7 +357,7 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
 #pragma unroll
                 for (int u = 0; u < kU; ++u) {
                     id[u] = src[u] != ~0ull ? nbr_in[src[u]] : 0u;
-                    wt[u] = (ew_out && src[u] != ~0ull) ? w_in[src[u]] : 0u;
+                    wt[u] = ((ew_out || pw_out) && src[u] != ~0ull) ? w_in[src[u]] : 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < kU; ++u) {
@@ -365,6 +367,10 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
                     const uint32_t y = new_id[id[u]];
                     if (nbr_out) nbr_out[x] = y;
                     if (ew_out) ew_out[x] = (uint64_t)y | ((uint64_t)wt[u] << 32);
+                    if (pw_out) {   // packed: the weight must fit the 32 - wshift high bits
+                        if ((uint64_t)wt[u] >> (32 - wshift)) *wbig = 1;
+                        pw_out[x] = y | (wt[u] << wshift);
+                    }
                 }
             }
             e = stop;
@@ -675,6 +681,17 @@ static void plan_phase(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off
     phase("hub sort + new offsets");
 }
 
+// bits of the largest vertex id (the shift of a packed record's weight)
+static uint32_t id_bits(uint64_t V) {
+    uint32_t b = 1;
+    while (b < 64 && (V - 1) >> b) ++b;
+    return b;
+}
+// packed SSSP records are tried when asked for and an id leaves >= 1 bit of a u32
+static bool pack_planned(const hyt_graph *g, uint64_t V, bool weighted) {
+    return weighted && g->prm.pack_weights && id_bits(V) < 32;
+}
+
 // The pinned mapped edge store of this rank's vertex range (the whole
 // graph at world 1), from a 16-byte chunk boundary, 16-B padded so chunk loads
 // never overrun.  row_start: null = full caller arrays (indexed by off_old),
@@ -691,7 +708,10 @@ static void rows_phase(hyt_graph *g, const uint64_t *row_start, const uint32_t *
     g->store_c0[1] = e_lo / 2;                          // first chunk of u64 records
     const uint64_t nbase = g->store_c0[0] * 4, wbase = g->store_c0[1] * 2;
     const uint64_t nbytes = (((e_hi - nbase) * 4 + 15) & ~15ull) + 32;
-    const uint64_t wbytes = (((e_hi - wbase) * 8 + 15) & ~15ull) + 32;
+    const bool pack = pack_planned(g, V, weighted);
+    // packed records share the ids' chunk geometry (4 B per edge)
+    const uint64_t wbytes = pack ? nbytes : (((e_hi - wbase) * 8 + 15) & ~15ull) + 32;
+    g->wshift = pack ? id_bits(V) : 0;
     if (adopt_ids) {
         g->nbr_h = const_cast<uint32_t *>(adopt_ids);
         g->nbr_adopted = true;
@@ -702,26 +722,32 @@ static void rows_phase(hyt_graph *g, const uint64_t *row_start, const uint32_t *
         HYT_REQUIRE((adopt_ids || nbytes == early->nbytes) && (!weighted || wbytes == early->wbytes), HYT_ESTATE,
                     "edge store size mismatch");
         if (!adopt_ids) { g->nbr_h = (uint32_t *)early->n; early->n = nullptr; }   // ownership moves
-        g->ew_h = (uint64_t *)early->w;
+        if (pack) g->pw_h = (uint32_t *)early->w;
+        else g->ew_h = (uint64_t *)early->w;
         early->w = nullptr;
     } else {
         if (!adopt_ids) g->nbr_h = (uint32_t *)pinned_alloc(nbytes);   // zero-filled (padding included)
-        if (weighted) g->ew_h = (uint64_t *)pinned_alloc(wbytes);
+        if (weighted && pack) g->pw_h = (uint32_t *)pinned_alloc(wbytes);
+        else if (weighted) g->ew_h = (uint64_t *)pinned_alloc(wbytes);
     }
     g->store_bytes = (adopt_ids ? 0 : nbytes) + (weighted ? wbytes : 0);
-    uint32_t *nbr_out = nullptr;
+    uint32_t *nbr_out = nullptr, *pw_out = nullptr;
     uint64_t *ew_out = nullptr;
     if (!adopt_ids) HYT_CUDA(cudaHostGetDevicePointer((void **)&nbr_out, g->nbr_h, 0));
-    if (weighted) HYT_CUDA(cudaHostGetDevicePointer((void **)&ew_out, g->ew_h, 0));
+    if (weighted && pack) HYT_CUDA(cudaHostGetDevicePointer((void **)&pw_out, g->pw_h, 0));
+    else if (weighted) HYT_CUDA(cudaHostGetDevicePointer((void **)&ew_out, g->ew_h, 0));
     phase("pin edge store");
     Temps T(g->arena);
     uint32_t *bad = (uint32_t *)T.get(16, "load: flag");
+    uint32_t *wbig = (uint32_t *)T.get(16, "load: weight flag");
     HYT_CUDA(cudaMemsetAsync(bad, 0, 4, st));
-    if (e_hi > e_lo && (nbr_out || ew_out || row_start)) {
+    HYT_CUDA(cudaMemsetAsync(wbig, 0, 4, st));
+    if (e_hi > e_lo && (nbr_out || ew_out || pw_out || row_start)) {
         k_relabel_tiles<<<num_sms() * 4, 512, 0, st>>>(V, e_lo, e_hi, g->ld_off_old, g->off_d, g->old_of_d, g->new_id_d,
                                                       row_start, g->store_v_lo, g->store_v_hi, nbr_dev, w_dev,
                                                       nbr_out ? nbr_out - nbase : nullptr,
-                                                      ew_out ? ew_out - wbase : nullptr, bad);
+                                                      ew_out ? ew_out - wbase : nullptr,
+                                                      pw_out ? pw_out - nbase : nullptr, g->wshift, wbig, bad);
     }
     if (g->off_h_pending) {   // the host offsets while the relabel kernel runs (its own stream)
         cudaStream_t side = nullptr;
@@ -736,6 +762,21 @@ static void rows_phase(hyt_graph *g, const uint64_t *row_start, const uint32_t *
     }
     HYT_REQUIRE(read_flag(bad, st) == 0, HYT_EINVAL, "neighbour id >= V");
     HYT_CUDA(cudaGetLastError());
+    if (pw_out && read_flag(wbig, st)) {
+        // a weight does not fit beside the id: the unpacked u64 records instead
+        pinned_free(g->pw_h);
+        g->pw_h = nullptr;
+        g->wshift = 0;
+        const uint64_t wb = (((e_hi - wbase) * 8 + 15) & ~15ull) + 32;
+        g->ew_h = (uint64_t *)pinned_alloc(wb);
+        g->store_bytes = (adopt_ids ? 0 : nbytes) + wb;
+        HYT_CUDA(cudaHostGetDevicePointer((void **)&ew_out, g->ew_h, 0));
+        k_relabel_tiles<<<num_sms() * 4, 512, 0, st>>>(V, e_lo, e_hi, g->ld_off_old, g->off_d, g->old_of_d, g->new_id_d,
+                                                      row_start, g->store_v_lo, g->store_v_hi, nbr_dev, w_dev,
+                                                      nullptr, ew_out - wbase, nullptr, 0, wbig, bad);
+        HYT_CUDA(cudaStreamSynchronize(st));
+        HYT_CUDA(cudaGetLastError());
+    }
     phase("relabel edges (zero-copy)");
 }
 
@@ -778,7 +819,7 @@ void load_graph(hyt_graph *g, uint64_t V, uint64_t E, const uint64_t *off, const
         const int dev = g->device;
         const bool weighted = w != nullptr;
         early.nbytes = ((E * 4 + 15) & ~15ull) + 32;
-        early.wbytes = ((E * 8 + 15) & ~15ull) + 32;
+        early.wbytes = pack_planned(g, V, weighted) ? early.nbytes : ((E * 8 + 15) & ~15ull) + 32;
         early.th = std::thread([&early, dev, weighted, adopt] {
             try {
                 cudaSetDevice(dev);

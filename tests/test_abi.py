@@ -78,9 +78,9 @@ def test_binding_constants_match_header():
     # hyt_iter: 3 u64 + 6 u32 + 3 u64 + 1 double; hyt_stats ends with pull_iters, um_balloon_bytes,
     # exch_peer, host_store_bytes
     assert ctypes.sizeof(hyt.hyt_iter) == 3 * 8 + 6 * 4 + 3 * 8 + 8
-    assert [f for f, _ in hyt.hyt_stats._fields_][-4:] == ["pull_iters", "um_balloon_bytes", "exch_peer",
-                                                           "host_store_bytes"]
-    assert "uint64_t host_store_bytes;" in txt
+    assert [f for f, _ in hyt.hyt_stats._fields_][-5:] == ["pull_iters", "um_balloon_bytes", "exch_peer",
+                                                           "host_store_bytes", "record_bytes"]
+    assert "uint64_t host_store_bytes;" in txt and "uint64_t record_bytes;" in txt
     assert "uint64_t pull_iters, um_balloon_bytes;" in txt and "uint32_t dir;" in txt
 
 

@@ -93,7 +93,7 @@ def test_multirank_budget_and_cache(hyt, algo):
     of its own partitions."""
     gkey = ("rmat", 13)
     g = gkey_graph(gkey)
-    d1 = 8 if algo == "sssp" else 4
+    d1 = 4          # ids, or SSSP records packed into 4 bytes (pack_weights)
     outs = run_ranks(hyt, g, algo, 2, part=4096, edge_cache=1, edge_cache_bytes=g.E * d1 // 4)
     check(gkey, algo, outs)
     assert sum(st["parts_resident"] for _, st in outs) > 0

@@ -200,7 +200,7 @@ def test_hub_sort_permutation_matches_oracle(hyt):
 
 
 @pytest.mark.parametrize("cost_model", [0, 1])
-@pytest.mark.parametrize("algo,d1", [("bfs", 4), ("sssp", 8)])
+@pytest.mark.parametrize("algo,d1", [("bfs", 4), ("sssp", 8), ("sssp", 4)])
 def test_plan_parity(hyt, algo, d1, cost_model):
     """the GPU's per-partition aggregates and engine choices equal the
     oracle's Algorithm 1 on the same frontier snapshot, bit-exact: with the paper's
@@ -217,6 +217,8 @@ def test_plan_parity(hyt, algo, d1, cost_model):
         rng = np.random.default_rng(7)
         G = hyt.Graph(device=0)
         try:
+            # SSSP records: 8 B (id, weight) or packed into 4 B (id | w << bits(V-1))
+            G.set("pack_weights", 1 if d1 == 4 else 0)
             G.load(g.off, g.nbr, g.w)
             G.set("cost_model", cost_model)
             if cost_model:
@@ -321,9 +323,10 @@ def test_partial_edge_cache(hyt, algo):
     device memory (engine R), the rest by the hybrid engines; results unchanged."""
     gkey = ("rmat", 9)
     g = symmetric_version(gkey) if algo == "cc" else gkey_graph(gkey)
-    d1 = 8 if algo == "sssp" else 4
+    d1 = 4          # ids, or SSSP records packed into 4 bytes (pack_weights, weights 1..63)
     # cache about half of the edge bytes: the rest still goes through the hybrid engines
     got, st, log = run_gpu(hyt, g, algo, part=4096, edge_cache=1, edge_cache_bytes=g.E * d1 // 2)
+    assert st["record_bytes"] == d1
     want = expected(gkey, algo)
     if algo == "pr":
         assert_pr_close(got, want)
@@ -436,3 +439,61 @@ def test_destination_bands(hyt, bands, algo):
                 assert_pr_close(got, want)
             else:
                 assert np.array_equal(got, want)
+
+
+def run_sssp_pack(hyt, g, pack, engine, part=4096, budget=0, **kw):
+    G = hyt.Graph(device=0, budget=budget)
+    try:
+        G.set("pack_weights", pack)          # load time: before hyt_load_csr
+        G.load(g.off, g.nbr, g.w)
+        G.set("engine_mode", engine)
+        G.set("partition_bytes", part)
+        for k, v in kw.items():
+            G.set(k, v)
+        G.run("sssp", src_of(g))
+        return G.values(), G.stats()
+    finally:
+        G.close()
+
+
+@pytest.mark.parametrize("pack", [0, 1])
+@pytest.mark.parametrize("engine", ENGINES + ["um"])
+@pytest.mark.parametrize("gkey", [("rmat", 4), ("rmat", 9), ("rmat", 13), ("crafted", 2), ("crafted", 5)],
+                         ids=lambda k: f"{k[0]}{k[1]}")
+def test_sssp_packed_records(hyt, pack, engine, gkey):
+    """pack_weights: SSSP over one u32 per edge (id | w << bits(V-1)) equals the
+    oracle bit for bit in every engine, and reads 4-byte records; pack_weights = 0
+    keeps the (id, w) u64 records."""
+    g = gkey_graph(gkey)
+    got, st = run_sssp_pack(hyt, g, pack, engine)
+    assert np.array_equal(got, expected(gkey, "sssp"))
+    assert st["record_bytes"] == (4 if pack else 8)
+
+
+@pytest.mark.parametrize("fits", [True, False])
+def test_sssp_pack_weight_limit(hyt, fits):
+    """Weights up to 2^(32 - bits(V-1)) - 1 pack; one larger weight makes the load fall
+    back to the u64 records -- both bit-exact against the oracle (the oracle sums in
+    u64, so distances stay exact)."""
+    V = 4096                                   # ids take 12 bits, weights get 20
+    g = hytgen.rmat_csr(12, V, 65536, seed=77, weighted=True)
+    w = np.asarray(g.w).copy()
+    rng = np.random.default_rng(5)
+    w[:] = rng.integers(1, 1 << 20, size=len(w), dtype=np.uint32)
+    if fits:
+        w[0] = (1 << 20) - 1
+    else:
+        w[len(w) // 2] = 1 << 20
+    g2 = hytgen.Graph(V=g.V, off=g.off, nbr=g.nbr, w=w, symmetric=False, name="wlimit")
+    want = oracle.sssp(g2.off, g2.nbr, g2.w, 0)
+    for engine in ("hybrid", "zerocopy", "resident"):
+        G = hyt.Graph(device=0)
+        try:
+            G.load(g2.off, g2.nbr, g2.w)
+            G.set("engine_mode", engine)
+            G.set("partition_bytes", 4096)
+            G.run("sssp", 0)
+            assert np.array_equal(G.values(), want), engine
+            assert G.stats()["record_bytes"] == (4 if fits else 8)
+        finally:
+            G.close()
