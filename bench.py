@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--budget-gb", type=float, default=16.0)
     ap.add_argument("--algos", default="sssp,pr")
     ap.add_argument("--engine", default="hybrid")
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-full", action="store_true", help="skip the full-size single-core oracle SSSP")
     ap.add_argument("--no-extras", action="store_true",
@@ -415,7 +415,7 @@ def run_extras(hyt, local: int, tw_graph=None) -> dict:
                 st = G.stats()
                 vals = G.values()
                 edges = reached_edges(g, vals) if a in ("sssp", "bfs") else g.E
-                d1 = 8 if a == "sssp" else 4
+                d1 = 8 if a == "sssp" else 4      # the paper's edge volume: (id, weight) = 8 B for SSSP
                 xfer = st["bytes_filter"] + st["bytes_compaction"] + st["bytes_zerocopy"]
                 if ref is None:
                     ref, agree = vals, True
@@ -424,7 +424,10 @@ def run_extras(hyt, local: int, tw_graph=None) -> dict:
                 else:
                     agree = bool(np.array_equal(vals, ref))
                 row[m] = {"s": sec, "gteps": edges / sec / 1e9, "iterations": int(st["iterations"]),
-                          "xfer_over_edge_volume": xfer / (g.E * d1), "agrees_with_hybrid": agree,
+                          "xfer_over_edge_volume": xfer / (g.E * d1),
+                          "record_bytes": int(st["record_bytes"]),
+                          "xfer_over_store_volume": xfer / (g.E * max(1, int(st["record_bytes"]))),
+                          "agrees_with_hybrid": agree,
                           "parts_fcz": [int(st["parts_filter"]), int(st["parts_compaction"]),
                                         int(st["parts_zerocopy"])]}
             if small:
@@ -606,6 +609,7 @@ def main():
         h2d = sum(a.nbytes for a in g.host_arrays() if a is not None)
         unpin_host(pinned)
         e2e = {"value": edges_step / (em / 1e3) / 1e9, "unit": "GTEPS", "ms_per_step": em,
+               "steps": len(e2e_ms), "step_ms": [float(x) for x in e2e_ms],
                "load_s": float(np.mean(e2e_load_s)),
                "inputs_pinned": len(pinned) == len([a for a in g.host_arrays() if a is not None]),
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * g.V * len(algos)),
