@@ -312,3 +312,33 @@ def test_calibrated_fig5():
     g3 = sum(zr for zr in [CAL.zr] * 3)
     assert g6 == 2 * g3
     assert oracle.select_cal(128, 64, 6, 6, 6, cfg, CAL) == oracle.select_cal(128, 64, 3, 3, 3, cfg, CAL) == oracle.Z
+
+
+@pytest.mark.parametrize("d1", [4, 8])
+@pytest.mark.parametrize("gamma_one", [False, True])
+def test_calibrated_rule_reduces_to_the_papers(d1, gamma_one):
+    """Pin of the calibrated rule against the PAPER's rule (oracle_select, itself pinned
+    by the SPEC worked examples): with no CPU term (link/Thpt_cpt = 0) and every
+    zero-copy request priced at 1/MR RTT (zr = zs = 1/MR), Tiz_cal = z/MR, which is the
+    paper's Tiz = ceil(z/MR) * (gamma + (1-gamma) e/t) whenever MR divides z and the
+    RTT_zc factor is 1 -- all edges of the partition active (e = t) or gamma = 1
+    (P:382-390).  On those inputs both rules must pick the same engine; a dropped or
+    mis-scaled term in either (the CPU term, the random/streamed split, the
+    thresholds) breaks the equality on some of the 20000 cases."""
+    rng = random.Random(7 + d1 + 10 * gamma_one)
+    cfg = oracle.CostCfg(d1=d1, gamma=Fraction(1) if gamma_one else Fraction(5, 8))
+    cal = oracle.Cal(Fraction(0), Fraction(1, cfg.mr), Fraction(1, cfg.mr))
+    counts = {0: 0, 1: 0, 2: 0, 3: 0}
+    for _ in range(20000):
+        t, e, a, z = random_case(rng, d1)
+        if not gamma_one:
+            e = t
+            a = max(a, 1) if t else 0
+        z = (z // cfg.mr) * cfg.mr                     # MR divides z: ceil(z/MR) = z/MR
+        r = min(a, z)
+        want = oracle.select(t, e, a, z, cfg)
+        assert oracle.select_cal(t, e, a, z, r, cfg, cal) == want, (t, e, a, z, r)
+        counts[want] += 1
+    assert min(counts[1], counts[3]) > 100
+    if gamma_one:                                      # with e = t, Tec >= Tef: never C
+        assert counts[2] > 100
