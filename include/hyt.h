@@ -244,7 +244,8 @@ int hyt_load_shard_rows(hyt_graph *g, uint64_t nrows, const uint64_t *row_off_ho
  *   the rates measured on the B200 pool are used and the run proceeds);
  *   0 is the paper's rule with its PCIe-3 constants.
  *   Kernel tuning (no effect on results): relax_ctas_per_sm [2] (in units of
- *   512 threads), zc_ctas_per_sm [1], relax_threads [0] (relax CTA size: 0 auto
+ *   512 threads), zc_ctas_per_sm [1], zc_ctas [0 = zc_ctas_per_sm x SMs]
+ *   (the zero-copy relax grid in 512-thread units), relax_threads [0] (relax CTA size: 0 auto
  *   = 1024 for PR, 512 otherwise; 512; 1024), relax_hot [1] (hub block ids <
  *   relax_hot_v in shared memory: PR delta accumulation in fixed point,
  *   min-algorithm value copy; 0 off, 1 auto, 2 always), relax_hot_v [16384]

@@ -133,6 +133,7 @@ int hyt_set_param(hyt_graph *g, const char *key, double v) {
         else if (k == "gather_threads") { integral(); in(0, 256); p.gather_threads = (int)v; }
         else if (k == "compaction_buffer_bytes") { integral(); in(0, 1e12); p.compaction_buffer_bytes = (uint64_t)v; }
         else if (k == "zc_ctas_per_sm") { integral(); in(1, 32); p.zc_ctas_per_sm = (int)v; }
+        else if (k == "zc_ctas") { integral(); in(0, 1 << 16); p.zc_ctas = (int)v; }
         else if (k == "relax_ctas_per_sm") { integral(); in(1, 32); p.relax_ctas_per_sm = (int)v; }
         else if (k == "exchange") { integral(); in(0, 3); p.exchange = (int)v; }
         else if (k == "relax_hot") { integral(); in(0, 2); p.relax_hot = (int)v; }

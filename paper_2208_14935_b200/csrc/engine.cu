@@ -925,7 +925,7 @@ void run_graph(hyt_graph *g, int algo, uint64_t source) {
     const int mode = P.engine_mode;
     const int prio = P.priority >= 0 ? P.priority : (algo == ALGO_PR ? 2 : 1);
     const int sms = num_sms();
-    const int relax_ctas = sms * P.relax_ctas_per_sm, zc_ctas = sms * P.zc_ctas_per_sm;
+    const int relax_ctas = sms * P.relax_ctas_per_sm, zc_ctas = P.zc_ctas > 0 ? P.zc_ctas : sms * P.zc_ctas_per_sm;
     const uint4 *edges_host = host_edges(g, c->algo);          // indexed by global chunk
     uint64_t store_c0 = 0;
     const void *store = edge_store(g, algo, &store_c0);

@@ -67,6 +67,7 @@ struct Params {
     int gather_threads = 0;
     uint64_t compaction_buffer_bytes = 0;
     int zc_ctas_per_sm = 1;     // 512-thread CTAs
+    int zc_ctas = 0;            // > 0: the zero-copy relax grid in 512-thread CTAs (overrides zc_ctas_per_sm)
     int relax_ctas_per_sm = 2;  // 512-thread CTAs
     int exchange = 1;          // multi-GPU: 0 dense, 1 sparse when cheaper (§8f #3), 2 sparse when it fits,
                                // 3 fused peer push (relax writes remote destinations into their owner's memory)

@@ -21,7 +21,7 @@ sys.path.insert(0, ROOT)
 DEFAULTS = {"relax_hot": 1, "relax_ctas_per_sm": 2, "zc_ctas_per_sm": 1, "edge_cache": 0, "relax_bands": 1,
             "relax_threads": 0, "relax_hot_v": 16384,
             "cost_model": 1, "recompute": 1, "priority": -1, "streams": 4, "k": 4, "exchange": 1,
-            "partition_bytes": 32 << 20, "epsilon": 1e-5}
+            "partition_bytes": 32 << 20, "epsilon": 1e-5, "zc_ctas": 0}
 
 
 def main():
