@@ -479,7 +479,7 @@ def main():
     # ---- inputs (host), generation not timed ----
     if world > 1:
         os.environ.setdefault("HYTGEN_THREADS", str(max(1, (os.cpu_count() or 8) // world)))
-    g = Workload(args.config, args.shift, True, world, rank, local, shard=multi)
+    g = Workload(args.config, args.shift, "sssp" in algos, world, rank, local, shard=multi)
     dstats = g.degree_stats()
 
     def new_handle():
