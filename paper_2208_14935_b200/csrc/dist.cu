@@ -163,6 +163,11 @@ void dist_share_ptrs(hyt_graph *g, void *const *mine, int nptr, void **all, std:
         return;
     }
     HYT_REQUIRE(g->nccl_comm, HYT_ESTATE, "peer exchange needs a multi-rank handle");
+    // a CUDA IPC handle maps its whole cudaMalloc block: the published arrays must be
+    // block bases, which holds for the library's own allocations but not for
+    // sub-allocations of a caller-provided arena (hyt_set_device_arena)
+    HYT_REQUIRE(!g->arena.ext, HYT_EINVAL,
+                "exchange = 3 across processes needs library-allocated device memory (no hyt_set_device_arena)");
     const uint64_t hb = sizeof(cudaIpcMemHandle_t);
     std::vector<cudaIpcMemHandle_t> h(nptr);
     for (int i = 0; i < nptr; ++i) HYT_CUDA(cudaIpcGetMemHandle(&h[i], mine[i]));
