@@ -344,7 +344,11 @@ int hyt_select_engine(const hyt_graph *g, uint64_t t, uint64_t e, uint64_t a, ui
  * pinned host memory only the edges of its own vertex range, about E/world of
  * them (hyt_rank_range).  It serves the partitions of that range.  Once per
  * iteration the ranks exchange pushed values: min for BFS/SSSP/CC, sum for PR
- * deltas.  Errors: HYT_ENCCL. */
+ * deltas.  world = 1 is allowed: the handle gets a one-rank communicator and
+ * takes the same multi-rank path (every collective an identity).  The fused
+ * peer push (exchange = 3) publishes CUDA IPC handles of the library's own
+ * device blocks and refuses a caller arena (hyt_set_device_arena).
+ * Errors: HYT_ENCCL, HYT_EINVAL. */
 int hyt_nccl_unique_id(void *uid_out_128_bytes);
 int hyt_init_dist(hyt_graph *g, int rank, int world, const void *nccl_uid_128_bytes);
 
