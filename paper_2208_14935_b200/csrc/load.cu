@@ -289,6 +289,28 @@ __global__ void k_finish_perm(uint64_t V, uint64_t h, const uint32_t *__restrict
 // are both coalesced (consecutive slots of a row are consecutive on both sides).
 constexpr int kRelabelTile = 8192, kRelabelRows = 2048;
 
+// 16-byte warp helpers of the relabel kernel: the next lane's vector, the r <= 3
+// values past a warp block (scalar loads of exactly those: nothing past the array),
+// and lane values r..r+3 of the concatenation (a, b).
+__device__ __forceinline__ uint4 shfl_down_u4(uint4 v) {
+    return make_uint4(__shfl_down_sync(FULL_MASK, v.x, 1), __shfl_down_sync(FULL_MASK, v.y, 1),
+                      __shfl_down_sync(FULL_MASK, v.z, 1), __shfl_down_sync(FULL_MASK, v.w, 1));
+}
+__device__ __forceinline__ uint4 tail_u4(const uint32_t *p, int r) {
+    return make_uint4(r > 0 ? p[0] : 0u, r > 1 ? p[1] : 0u, r > 2 ? p[2] : 0u, 0u);
+}
+__device__ __forceinline__ void pick4(const uint4 &a, const uint4 &b, int r, uint32_t *o) {
+    const uint32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        uint32_t x = c[k];
+#pragma unroll
+        for (int q = 1; q < 4; ++q)
+            if (r == q) x = c[k + q];
+        o[k] = x;
+    }
+}
+
 // row_start (shard loads): the first edge of internal row r in the caller's local
 // arrays is row_start[r - r_base] (rows r_base..r_end-1 only); otherwise it is
 // off_old[old_of[r]] in the caller's full arrays.  A neighbour id >= V sets *bad.
@@ -334,42 +356,88 @@ k_relabel_tiles(uint64_t V, uint64_t e_lo, uint64_t e_hi, const uint64_t *__rest
             }
             __syncthreads();
             const uint64_t stop = min(e_end, s_new[nr]);   // edges the staged rows cover
-            // kU coalesced slots per thread per round, all loads issued before any use:
-            // the caller's arrays are read over the host link, where one 4-byte load in
-            // flight per thread leaves the link idle
-            constexpr int kU = 4;
-            for (uint64_t x0 = e + threadIdx.x; x0 < stop; x0 += (uint64_t)kU * blockDim.x) {
-                uint64_t src[kU];
-                uint32_t id[kU], wt[kU];
+            // Warp blocks of 128 consecutive slots, 4 per lane.  Stores: one 16-byte
+            // store per lane whenever its 4 slots are all in range (x % 4 == 0, and the
+            // stores are chunk-aligned).  Loads: when the block's 128 slots come from
+            // 128 consecutive source edges (one shift; the common case, since non-hub
+            // rows keep their order), each lane reads 16 aligned bytes and takes its 4
+            // values across its own and the next lane's vector; otherwise 4 scalar
+            // loads per lane.  The caller's arrays are read over the host link.
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+            const bool vec_in = ((((uintptr_t)nbr_in) | (w_in ? (uintptr_t)w_in : 0)) & 15) == 0;
+            const bool need_w = ew_out || pw_out;
+            for (uint64_t xb = (e & ~127ull) + (uint64_t)warp * 128; xb < stop; xb += (uint64_t)nwarps * 128) {
+                const uint64_t xl = xb + 4ull * lane;
+                uint64_t src[4];
+                bool val[4];
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const uint64_t x = x0 + (uint64_t)u * blockDim.x;
-                    src[u] = ~0ull;
-                    if (x < stop) {
+                for (int k = 0; k < 4; ++k) {
+                    const uint64_t x = xl + k;
+                    val[k] = x >= e && x < stop;
+                    src[k] = 0;
+                    if (val[k]) {
                         int lo = 0, hi = (int)nr - 1;      // last staged row starting <= x
                         while (lo < hi) {
                             const int mid = (lo + hi + 1) >> 1;
                             if (s_new[mid] <= x) lo = mid; else hi = mid - 1;
                         }
-                        src[u] = s_old[lo] + (x - s_new[lo]);
+                        src[k] = s_old[lo] + (x - s_new[lo]);
                     }
                 }
+                const bool full = val[0] && val[1] && val[2] && val[3];
+                const uint64_t shift = src[0] - xl;       // source - slot (mod 2^64)
+                const bool mine = full && src[1] == src[0] + 1 && src[2] == src[0] + 2 && src[3] == src[0] + 3;
+                const uint64_t shift0 = __shfl_sync(FULL_MASK, shift, 0);
+                const bool uni = vec_in && __all_sync(FULL_MASK, mine && shift == shift0);
+                uint32_t id[4], wt[4] = {0u, 0u, 0u, 0u};
+                if (uni) {
+                    const uint64_t s0 = xb + shift0, a = s0 & ~3ull;
+                    const int r = (int)(s0 - a);
+                    uint4 v = reinterpret_cast<const uint4 *>(nbr_in + a)[lane];
+                    uint4 vn = shfl_down_u4(v);
+                    if (lane == 31) vn = tail_u4(nbr_in + a + 128, r);
+                    pick4(v, vn, r, id);
+                    if (need_w) {
+                        uint4 w4 = reinterpret_cast<const uint4 *>(w_in + a)[lane];
+                        uint4 wn = shfl_down_u4(w4);
+                        if (lane == 31) wn = tail_u4(w_in + a + 128, r);
+                        pick4(w4, wn, r, wt);
+                    }
+                } else {
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    id[u] = src[u] != ~0ull ? nbr_in[src[u]] : 0u;
-                    wt[u] = ((ew_out || pw_out) && src[u] != ~0ull) ? w_in[src[u]] : 0u;
+                    for (int k = 0; k < 4; ++k) {
+                        id[k] = val[k] ? nbr_in[src[k]] : 0u;
+                        if (need_w && val[k]) wt[k] = w_in[src[k]];
+                    }
                 }
+                uint32_t y[4];
 #pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    if (src[u] == ~0ull) continue;
-                    const uint64_t x = x0 + (uint64_t)u * blockDim.x;
-                    if (id[u] >= V) { *bad = 1; continue; }
-                    const uint32_t y = new_id[id[u]];
-                    if (nbr_out) nbr_out[x] = y;
-                    if (ew_out) ew_out[x] = (uint64_t)y | ((uint64_t)wt[u] << 32);
-                    if (pw_out) {   // packed: the weight must fit the 32 - wshift high bits
-                        if ((uint64_t)wt[u] >> (32 - wshift)) *wbig = 1;
-                        pw_out[x] = y | (wt[u] << wshift);
+                for (int k = 0; k < 4; ++k) {
+                    y[k] = 0u;
+                    if (!val[k]) continue;
+                    if (id[k] >= V) { *bad = 1; continue; }
+                    y[k] = new_id[id[k]];
+                    if (pw_out && ((uint64_t)wt[k] >> (32 - wshift))) *wbig = 1;
+                }
+                if (full) {
+                    if (nbr_out) *reinterpret_cast<uint4 *>(nbr_out + xl) = make_uint4(y[0], y[1], y[2], y[3]);
+                    if (pw_out)
+                        *reinterpret_cast<uint4 *>(pw_out + xl) =
+                            make_uint4(y[0] | (wt[0] << wshift), y[1] | (wt[1] << wshift), y[2] | (wt[2] << wshift),
+                                       y[3] | (wt[3] << wshift));
+                    if (ew_out) {
+                        uint4 *o = reinterpret_cast<uint4 *>(ew_out + xl);
+                        o[0] = make_uint4(y[0], wt[0], y[1], wt[1]);
+                        o[1] = make_uint4(y[2], wt[2], y[3], wt[3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (!val[k] || id[k] >= V) continue;
+                        const uint64_t x = xl + k;
+                        if (nbr_out) nbr_out[x] = y[k];
+                        if (ew_out) ew_out[x] = (uint64_t)y[k] | ((uint64_t)wt[k] << 32);
+                        if (pw_out) pw_out[x] = y[k] | (wt[k] << wshift);
                     }
                 }
             }
